@@ -1,0 +1,146 @@
+/*
+ * heb200.h -- C ABI of the B200 CKKS evaluation engine (libheb200.so).
+ *
+ * The drop-in boundary for the reference's HE backend plugin
+ * (/root/reference/pkg/src/hecnn/backends/base.py:190-602, hooks :554-602).
+ * Plain pointers and sizes only; every call returns 0 on success or a
+ * negative HEB_E* status, with a message in heb_last_error() (thread-local).
+ *
+ * Data layout (device memory, u64 words):
+ *   a "row" is N residues of one prime; residues are x*2^64 mod p in [0,p)
+ *   ("Montgomery form", reference kernels.py:1-13), evaluation (NTT) domain,
+ *   position i = a(psi^(2*brv(i)+1)).
+ *   A ciphertext batch operand heb_ct points at component 0 / row 0 of item 0;
+ *   item b, component c, row r lives at data + b*ct_stride + c*comp_stride + r*N.
+ *   Rows are the prefix 0..level of the context's primes (row 0 = base prime).
+ *   Raw products (degree 2) use the same descriptor with three components.
+ * All work is enqueued on `stream` (a cudaStream_t, may be NULL); temporary
+ * device memory is stream-ordered (cudaMallocAsync), so independent calls may
+ * use independent streams.
+ */
+#ifndef HEB200_H
+#define HEB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HEB_OK 0
+#define HEB_EINVAL (-1)   /* bad argument (maps to ValueError) */
+#define HEB_ECUDA (-2)    /* CUDA runtime/launch failure (DeviceError) */
+#define HEB_ENOMEM (-3)   /* device allocation failed (DeviceError) */
+#define HEB_EUNSUP (-4)   /* ring degree / shape not supported (ConfigurationError) */
+
+typedef struct heb_ctx heb_ctx;
+
+typedef struct heb_ct {
+    uint64_t *data;
+    int64_t ct_stride;    /* words between batch items */
+    int64_t comp_stride;  /* words between components (c0/c1 or d0/d1/d2) */
+} heb_ct;
+
+/* --- library / context ---------------------------------------------------- */
+int heb_version(void);
+const char *heb_last_error(void);
+int heb_device_count(int *count);
+
+/* Build the device tables for one modulus chain.  primes[num_rows] in chain row
+ * order (base, levels..., special) -- reference chain.py:26-31; psi[] holds each
+ * prime's 2N-th root from find_2n_root (kernels.py:439-446) or NULL to derive it.
+ * Replaces the per-backend precomputation in ckks.py:81-93 / chain.py:97-147. */
+int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows, const uint64_t *primes,
+                   const uint64_t *psi);
+int heb_ctx_destroy(heb_ctx *ctx);
+int heb_ctx_ring_degree(const heb_ctx *ctx);
+/* Key-switch batches are processed in chunks of this many items so the
+ * intermediates stay L2-resident (default 64). */
+int heb_ctx_set_chunk(heb_ctx *ctx, int items);
+
+/* --- memory ----------------------------------------------------------------- */
+int heb_alloc(size_t bytes, void **out, void *stream);
+int heb_free(void *ptr, void *stream);
+int heb_h2d(void *dst, const void *src, size_t bytes, void *stream);
+int heb_d2h(void *dst, const void *src, size_t bytes, void *stream);
+int heb_sync(void *stream);
+
+/* --- transforms (kernels.py:68-114) ------------------------------------------ */
+/* In place over `count` blocks of `rows` rows starting at chain row `row0`. */
+int heb_ntt_fwd(heb_ctx *ctx, uint64_t *data, int64_t count, int rows, int row0, int64_t block_stride,
+                void *stream);
+int heb_ntt_inv(heb_ctx *ctx, uint64_t *data, int64_t count, int rows, int row0, int64_t block_stride,
+                void *stream);
+/* Centered int64 coefficients (count, N) -> evaluation rows 0..rows-1 (Montgomery).
+ * Restates spread_centered + ntt_fwd_rows (ckks.py:120-126). If `all_with_special`
+ * is nonzero, the row set is every chain row (keygen, ckks.py:128-129). */
+int heb_spread_ntt(heb_ctx *ctx, const int64_t *coeffs, int64_t count, uint64_t *out, int rows,
+                   int64_t out_stride, void *stream);
+
+/* --- arithmetic (ckks.py:279-387) --------------------------------------------- */
+/* out = a + b over `comps` components of k rows (add_ct_ct / raw_add). */
+int heb_add(heb_ctx *ctx, heb_ct a, heb_ct b, heb_ct out, int64_t count, int comps, int k, void *stream);
+/* out.c0 = ct.c0 + pt (pt: k rows, item stride pt_stride; 0 = broadcast); c1 copied
+ * unless out aliases ct (add_ct_pt, ckks.py:295-302). */
+int heb_add_plain(heb_ctx *ctx, heb_ct ct, const uint64_t *pt, int64_t pt_stride, heb_ct out, int64_t count,
+                  int k, void *stream);
+/* raw (d0,d1,d2) (+)= (a0b0, a0b1+a1b0, a1b1)  (ctct_products, kernels.py:230-246). */
+int heb_tensor(heb_ctx *ctx, heb_ct a, heb_ct b, heb_ct raw, int64_t count, int k, int accumulate,
+               void *stream);
+/* Rescale `comps` components at `level` (k = level+1 rows -> k-1): divide_drop_last,
+ * kernels.py:270-294.  If pt != NULL each component is first multiplied by the
+ * plaintext rows (mul_ct_pt = mul_rows + rescale, ckks.py:320-331). */
+int heb_rescale(heb_ctx *ctx, heb_ct in, const uint64_t *pt, int64_t pt_stride, heb_ct out, int64_t count,
+                int comps, int level, void *stream);
+/* raw_finalize (ckks.py:359-387): key switch of d2 with the relinearisation key
+ * (relin_accumulate + moddown_special), add d0/d1, rescale.  evk_b/evk_a are the
+ * reference EvalKeyPayload arrays (digits, num_rows, N). Output level = level-1. */
+int heb_relin_rescale(heb_ctx *ctx, heb_ct raw, const uint64_t *evk_b, const uint64_t *evk_a, heb_ct out,
+                      int64_t count, int level, void *stream);
+/* Galois automorphism X -> X^galois on both components followed by a key switch
+ * with the matching switching key (same layout as evk); level kept.  No reference
+ * counterpart (rotation is a non-goal there). */
+int heb_rotate(heb_ctx *ctx, heb_ct ct, const uint64_t *gk_b, const uint64_t *gk_a, heb_ct out, int64_t count,
+               int level, uint64_t galois, void *stream);
+/* Evaluation-domain permutation only (rows 0..rows-1 of `count` blocks). */
+int heb_galois(heb_ctx *ctx, const uint64_t *in, uint64_t *out, int64_t count, int rows, int64_t block_stride,
+               uint64_t galois, void *stream);
+/* out = a (*) b pointwise Montgomery product over `rows` rows (mul_rows). */
+int heb_mul_rows(heb_ctx *ctx, const uint64_t *a, const uint64_t *b, uint64_t *out, int rows, void *stream);
+
+/* --- client side (ckks.py:135-273) ------------------------------------------------ */
+/* Encrypt `count` messages: c0 = v*pk_b + (e0+m), c1 = v*pk_a + e1 over k rows.
+ * v, e0m, e1: int64 coefficient vectors (count, N) sampled on the host. */
+int heb_encrypt(heb_ctx *ctx, const int64_t *v, const int64_t *e0m, const int64_t *e1, const uint64_t *pk_b,
+                const uint64_t *pk_a, heb_ct out, int64_t count, int k, void *stream);
+/* Decrypt to centered int64 coefficients of row 0 with the cross-residue guard
+ * (ckks.py:237-269): bad[b] = number of coefficients whose residue mod q_1 differs
+ * from row 1 (k >= 2), or of coefficients >= q_0/4 in magnitude (k == 1). */
+int heb_decrypt(heb_ctx *ctx, heb_ct ct, const uint64_t *s_eval, int64_t *coeffs, int64_t *bad, int64_t count,
+                int k, void *stream);
+/* pk_b = e - a*s over `rows` rows (keygen, ckks.py:143-149). */
+int heb_make_public_key(heb_ctx *ctx, const uint64_t *s_eval, const uint64_t *a, const int64_t *e,
+                        uint64_t *pk_b, int rows, void *stream);
+/* Switching key: for digit j < digits, kb[j] = e_j - a_j*s (all rows) and row j gets
+ * + (P mod q_j) * target[j] (ckks.py:151-176; target = s^2 for relinearisation,
+ * sigma_g(s) for rotation). */
+int heb_make_switch_key(heb_ctx *ctx, const uint64_t *s_eval, const uint64_t *target, const uint64_t *a,
+                        const int64_t *e, uint64_t *kb, int digits, void *stream);
+
+/* --- batched layer evaluator (layers.py:92-294 fused per layer) --------------------- */
+/* For output o < n_out: raw_o = sum_{t<taps} A[a_idx[o*taps+t]] (x) B[b_idx[o*taps+t]]
+ * (degree-2 tensor, lazy 128-bit accumulation); index arrays are device int32. */
+int heb_dot_tensor(heb_ctx *ctx, heb_ct a, heb_ct b, const int32_t *a_idx, const int32_t *b_idx, int taps,
+                   heb_ct raw, int64_t n_out, int k, void *stream);
+/* out_o = sum_{t<terms} A[idx[o*terms+t]] over `comps` components (pool windows). */
+int heb_sum_gather(heb_ctx *ctx, heb_ct a, const int32_t *idx, int terms, heb_ct out, int64_t n_out, int comps,
+                   int k, void *stream);
+/* out_o = A[idx[o]] (gather copy of k rows x comps). */
+int heb_gather(heb_ctx *ctx, heb_ct a, const int32_t *idx, heb_ct out, int64_t n_out, int comps, int k,
+               void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEB200_H */

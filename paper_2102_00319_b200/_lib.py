@@ -1,0 +1,102 @@
+"""ctypes binding of libheb200.so (the C ABI declared in include/heb200.h).
+
+The product path has no CPU fallback: if the library or a CUDA device is
+missing, ``lib()`` raises ``DeviceError`` immediately.  Status codes map onto
+the reference error taxonomy (`hecnn/errors.py`).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import ConfigurationError, DeviceError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libheb200.so")
+
+
+class HebCt(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("ct_stride", ctypes.c_int64), ("comp_stride", ctypes.c_int64)]
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_L = ctypes.c_int64
+_U = ctypes.c_uint64
+_CT = HebCt
+
+# name -> argtypes (all return int status unless listed in _RET)
+SIGNATURES: dict[str, list] = {
+    "heb_version": [],
+    "heb_last_error": [],
+    "heb_device_count": [ctypes.POINTER(ctypes.c_int)],
+    "heb_ctx_create": [ctypes.POINTER(_P), _I, _I, _I, _P, _P],
+    "heb_ctx_destroy": [_P],
+    "heb_ctx_ring_degree": [_P],
+    "heb_ctx_set_chunk": [_P, _I],
+    "heb_alloc": [ctypes.c_size_t, ctypes.POINTER(_P), _P],
+    "heb_free": [_P, _P],
+    "heb_h2d": [_P, _P, ctypes.c_size_t, _P],
+    "heb_d2h": [_P, _P, ctypes.c_size_t, _P],
+    "heb_sync": [_P],
+    "heb_ntt_fwd": [_P, _P, _L, _I, _I, _L, _P],
+    "heb_ntt_inv": [_P, _P, _L, _I, _I, _L, _P],
+    "heb_spread_ntt": [_P, _P, _L, _P, _I, _L, _P],
+    "heb_add": [_P, _CT, _CT, _CT, _L, _I, _I, _P],
+    "heb_add_plain": [_P, _CT, _P, _L, _CT, _L, _I, _P],
+    "heb_tensor": [_P, _CT, _CT, _CT, _L, _I, _I, _P],
+    "heb_rescale": [_P, _CT, _P, _L, _CT, _L, _I, _I, _P],
+    "heb_relin_rescale": [_P, _CT, _P, _P, _CT, _L, _I, _P],
+    "heb_rotate": [_P, _CT, _P, _P, _CT, _L, _I, _U, _P],
+    "heb_galois": [_P, _P, _P, _L, _I, _L, _U, _P],
+    "heb_mul_rows": [_P, _P, _P, _P, _I, _P],
+    "heb_encrypt": [_P, _P, _P, _P, _P, _P, _CT, _L, _I, _P],
+    "heb_decrypt": [_P, _CT, _P, _P, _P, _L, _I, _P],
+    "heb_make_public_key": [_P, _P, _P, _P, _P, _I, _P],
+    "heb_make_switch_key": [_P, _P, _P, _P, _P, _P, _I, _P],
+    "heb_dot_tensor": [_P, _CT, _CT, _P, _P, _I, _CT, _L, _I, _P],
+    "heb_sum_gather": [_P, _CT, _P, _I, _CT, _L, _I, _I, _P],
+    "heb_gather": [_P, _CT, _P, _CT, _L, _I, _I, _P],
+}
+_RET = {"heb_last_error": ctypes.c_char_p, "heb_version": ctypes.c_int, "heb_ctx_ring_degree": ctypes.c_int}
+
+_lock = threading.Lock()
+_LIB: ctypes.CDLL | None = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """dlopen the library and declare every exported entry point."""
+    if not os.path.exists(path):
+        raise DeviceError(f"CUDA library not built: {path} (run paper_2102_00319_b200.build)")
+    lib = ctypes.CDLL(path)
+    for name, args in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _RET.get(name, ctypes.c_int)
+    return lib
+
+
+def lib() -> ctypes.CDLL:
+    global _LIB
+    with _lock:
+        if _LIB is None:
+            _LIB = load()
+        return _LIB
+
+
+def check(status: int, what: str = "") -> None:
+    if status == 0:
+        return
+    msg = (lib().heb_last_error() or b"").decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if status == -1:
+        raise ValueError(text)
+    if status == -4:
+        raise ConfigurationError(text)
+    raise DeviceError(text)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args), name)

@@ -1,0 +1,159 @@
+// common.cuh -- shared declarations of the libheb200 translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/heb200.h"
+#include "modarith.cuh"
+#include "ntt.cuh"
+
+typedef unsigned __int128 u128;
+
+int fail(int code, const char *fmt, ...);
+
+#define CUDA_TRY(expr)                                                                     \
+    do {                                                                                   \
+        cudaError_t _e = (expr);                                                           \
+        if (_e != cudaSuccess)                                                             \
+            return fail(HEB_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), \
+                        __FILE__, __LINE__);                                               \
+    } while (0)
+
+#define LAUNCH_CHECK() CUDA_TRY(cudaGetLastError())
+
+// =============================================================================
+// context
+// =============================================================================
+struct LevelConst {
+    // rescale at this level drops q_L (row `level`); valid for rows i < level
+    ulonglong2 beta, beta_r;     // q_L^-1, q_L^-1 * R            (mod q_i)
+    ulonglong2 alpha, alpha_r;   // P^-1 q_L^-1, P^-1 q_L^-1 R    (mod q_i)
+    // key switch at this level (rows i <= level) and the q_L row's own constants
+    ulonglong2 gamma, gamma_r;   // P^-1, P^-1 R                  (mod q_i)
+    ulonglong2 pmod, pinv;       // P mod q_i, P^-1 mod q_i       (std)
+};
+
+struct LastConst {  // final inverse-stage factors (Shoup pairs)
+    ulonglong2 u_plain, v_plain;  // n^-1,       itw[1] n^-1
+    ulonglong2 u_std, v_std;      // n^-1 R^-1,  itw[1] n^-1 R^-1  (fold from-Montgomery)
+};
+
+struct heb_ctx {
+    int device = 0, log_n = 0, n = 0, num_rows = 0, chunk = 64;
+    std::vector<u64> primes;
+    PrimeInfo *d_pi = nullptr;
+    ulonglong2 *d_tw = nullptr, *d_itw = nullptr;
+    LevelConst *d_lc = nullptr;
+    LastConst *d_last = nullptr;
+    int flush = 64;  // lazy 128-bit accumulation: products summed before a reduction
+};
+
+// scoped stream-ordered scratch
+struct Scratch {
+    void *p = nullptr;
+    cudaStream_t s;
+    explicit Scratch(cudaStream_t st) : s(st) {}
+    cudaError_t get(size_t bytes) { return cudaMallocAsync(&p, bytes ? bytes : 8, s); }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
+// =============================================================================
+// device helpers
+// =============================================================================
+struct Ctx {  // kernel-side view of the context
+    const PrimeInfo *pi;
+    const ulonglong2 *tw, *itw;
+    const LevelConst *lc;
+    const LastConst *last;
+    int num_rows;
+};
+static inline Ctx kctx(const heb_ctx *c) { return Ctx{c->d_pi, c->d_tw, c->d_itw, c->d_lc, c->d_last, c->num_rows}; }
+
+template <int LOGN>
+__device__ __forceinline__ const ulonglong2 *tw_row(const Ctx &k, int row) {
+    return k.tw + ((size_t)row << LOGN);
+}
+template <int LOGN>
+__device__ __forceinline__ const ulonglong2 *itw_row(const Ctx &k, int row) {
+    return k.itw + ((size_t)row << LOGN);
+}
+
+// thread's 16 contiguous positions: vectorised load/store
+__device__ __forceinline__ void load16(const u64 *__restrict__ src, u64 (&v)[16]) {
+    const ulonglong2 *s = reinterpret_cast<const ulonglong2 *>(src);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        ulonglong2 t = s[i];
+        v[2 * i] = t.x;
+        v[2 * i + 1] = t.y;
+    }
+}
+__device__ __forceinline__ void store16(u64 *__restrict__ dst, const u64 (&v)[16]) {
+    ulonglong2 *d = reinterpret_cast<ulonglong2 *>(dst);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i] = make_ulonglong2(v[2 * i], v[2 * i + 1]);
+}
+
+template <int LOGN>
+static constexpr size_t smem_bytes() {
+    return sizeof(u64) * ntt::Shape<LOGN>::SMEM_WORDS;
+}
+
+template <class K>
+static cudaError_t prep_kernel(K kernel, size_t smem) {
+    if (smem > 48 * 1024)
+        return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return cudaSuccess;
+}
+
+#define DISPATCH_LOGN(ctx, FN, ...)                                          \
+    switch ((ctx)->log_n) {                                                  \
+        case 6: return FN<6>(__VA_ARGS__);                                   \
+        case 7: return FN<7>(__VA_ARGS__);                                   \
+        case 8: return FN<8>(__VA_ARGS__);                                   \
+        case 9: return FN<9>(__VA_ARGS__);                                   \
+        case 10: return FN<10>(__VA_ARGS__);                                 \
+        case 11: return FN<11>(__VA_ARGS__);                                 \
+        case 12: return FN<12>(__VA_ARGS__);                                 \
+        case 13: return FN<13>(__VA_ARGS__);                                 \
+        case 14: return FN<14>(__VA_ARGS__);                                 \
+        default: return fail(HEB_EUNSUP, "unsupported log_n %d", (ctx)->log_n); \
+    }
+
+static inline unsigned gdim(int64_t v) { return (unsigned)(v < 65535 ? (v < 1 ? 1 : v) : 65535); }
+
+// =============================================================================
+// pointwise kernels (HBM-bound)
+// =============================================================================
+// grid.y enumerates (item, comp, row) "lines"; grid.x * block covers N.
+struct LineIdx {
+    int64_t b;
+    int c, r;
+};
+__device__ __forceinline__ LineIdx line_of(int64_t line, int comps, int k) {
+    LineIdx L;
+    L.r = (int)(line % k);
+    int64_t t = line / k;
+    L.c = (int)(t % comps);
+    L.b = t / comps;
+    return L;
+}
+__device__ __forceinline__ u64 *at(const heb_ct &x, int64_t b, int c, int r, int logn) {
+    return x.data + b * x.ct_stride + c * x.comp_stride + ((int64_t)r << logn);
+}
+
+
+static inline dim3 pw_grid(int n, int64_t lines) {
+    int bx = (n + 255) / 256;
+    return dim3(bx, gdim(lines));
+}
+
+__global__ void k_galois_ct(heb_ct in, heb_ct out, int64_t lines, int k, int logn, u64 g);

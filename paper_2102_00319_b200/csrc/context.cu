@@ -1,0 +1,215 @@
+// context.cu -- error state, host-side number theory, context tables, memory API.
+#include "common.cuh"
+
+static thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+// =============================================================================
+// host-side number theory (cold path, exact 128-bit arithmetic)
+// =============================================================================
+static u64 mulmod_h(u64 a, u64 b, u64 p) { return (u64)((u128)a * b % p); }
+static u64 powmod_h(u64 a, u64 e, u64 p) {
+    u64 r = 1 % p;
+    a %= p;
+    while (e) {
+        if (e & 1) r = mulmod_h(r, a, p);
+        a = mulmod_h(a, a, p);
+        e >>= 1;
+    }
+    return r;
+}
+static u64 invmod_h(u64 a, u64 p) { return powmod_h(a, p - 2, p); }  // p prime
+static u64 shoup_companion(u64 w, u64 p) { return (u64)(((u128)w << 64) / p); }
+static ulonglong2 shoup_pair(u64 w, u64 p) {
+    ulonglong2 r;
+    r.x = w % p;
+    r.y = shoup_companion(r.x, p);
+    return r;
+}
+static u64 r_mod(u64 p) { return (u64)(((u128)1 << 64) % p); }
+static u64 neg_inv64(u64 p) {
+    u64 x = p;  // Newton iteration for p^-1 mod 2^64
+    for (int i = 0; i < 6; ++i) x *= 2 - p * x;
+    return (u64)0 - x;
+}
+// first element of exact order 2n (reference kernels.py:439-446)
+static u64 find_2n_root_h(u64 n, u64 p) {
+    u64 e = (p - 1) / (2 * n);
+    for (u64 x = 2; x < (1u << 20); ++x) {
+        u64 y = powmod_h(x, e, p);
+        if (powmod_h(y, n, p) == p - 1) return y;
+    }
+    return 0;
+}
+static u32 brv_h(u32 x, int bits) {
+    u32 y = 0;
+    for (int i = 0; i < bits; ++i) y |= ((x >> i) & 1u) << (bits - 1 - i);
+    return y;
+}
+
+extern "C" int heb_version(void) { return 1; }
+extern "C" const char *heb_last_error(void) { return g_err.c_str(); }
+extern "C" int heb_device_count(int *count) {
+    CUDA_TRY(cudaGetDeviceCount(count));
+    return HEB_OK;
+}
+
+extern "C" int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows, const uint64_t *primes,
+                              const uint64_t *psi) {
+    if (!out || !primes || num_rows < 2) return fail(HEB_EINVAL, "heb_ctx_create: bad arguments");
+    if (log_n < 6 || log_n > 14) return fail(HEB_EUNSUP, "ring degree 2^%d not supported (2^6 .. 2^14)", log_n);
+    const int n = 1 << log_n;
+    auto *c = new heb_ctx();
+    c->device = device;
+    c->log_n = log_n;
+    c->n = n;
+    c->num_rows = num_rows;
+    c->primes.assign(primes, primes + num_rows);
+    u64 pmax = 0;
+    for (u64 p : c->primes) {
+        if (p >= (1ull << 62) || p % (2ull * n) != 1) {
+            delete c;
+            return fail(HEB_EINVAL, "prime %llu is not an NTT prime < 2^62 for n=%d", (unsigned long long)p, n);
+        }
+        pmax = p > pmax ? p : pmax;
+    }
+    // products of canonical residues are < p^2; allow as many in a 128-bit accumulator
+    {
+        u128 lim = (~(u128)0) / ((u128)pmax * pmax);
+        c->flush = lim > 64 ? 64 : (int)lim;
+    }
+    std::vector<PrimeInfo> pi(num_rows);
+    std::vector<ulonglong2> tw((size_t)num_rows * n), itw((size_t)num_rows * n);
+    std::vector<LastConst> last(num_rows);
+    for (int r = 0; r < num_rows; ++r) {
+        const u64 p = c->primes[r];
+        const u64 g = psi ? psi[r] : find_2n_root_h(n, p);
+        if (!g || powmod_h(g, n, p) != p - 1) {
+            delete c;
+            return fail(HEB_EINVAL, "psi for prime %llu has wrong order", (unsigned long long)p);
+        }
+        PrimeInfo &q = pi[r];
+        memset(&q, 0, sizeof q);
+        q.p = p;
+        q.pinv = neg_inv64(p);
+        q.r1s = shoup_companion(1, p);
+        q.rmod = r_mod(p);
+        q.rmod_s = shoup_companion(q.rmod, p);
+        q.rinv = invmod_h(q.rmod, p);
+        q.rinv_s = shoup_companion(q.rinv, p);
+        q.ninv = invmod_h((u64)n % p, p);
+        q.ninv_s = shoup_companion(q.ninv, p);
+        q.ninv_rinv = mulmod_h(q.ninv, q.rinv, p);
+        q.ninv_rinv_s = shoup_companion(q.ninv_rinv, p);
+        // powers of psi in bit-reversed order: tw[i] = psi^brv(i)   (kernels.py:464-475, std form)
+        std::vector<u64> pw(n);
+        pw[0] = 1;
+        for (int i = 1; i < n; ++i) pw[i] = mulmod_h(pw[i - 1], g, p);
+        for (int i = 0; i < n; ++i) {
+            u64 w = pw[brv_h((u32)i, log_n)];
+            tw[(size_t)r * n + i] = shoup_pair(w, p);
+            itw[(size_t)r * n + i] = shoup_pair(invmod_h(w, p), p);
+        }
+        const u64 it1 = itw[(size_t)r * n + 1].x;
+        last[r].u_plain = shoup_pair(q.ninv, p);
+        last[r].v_plain = shoup_pair(mulmod_h(it1, q.ninv, p), p);
+        last[r].u_std = shoup_pair(q.ninv_rinv, p);
+        last[r].v_std = shoup_pair(mulmod_h(it1, q.ninv_rinv, p), p);
+    }
+    // per-level constants; P = special prime (last row)
+    const int levels = num_rows - 1;  // level 0 .. num_rows-2
+    const u64 P = c->primes[num_rows - 1];
+    std::vector<LevelConst> lc((size_t)levels * num_rows);
+    memset(lc.data(), 0, lc.size() * sizeof(LevelConst));
+    for (int lvl = 0; lvl < levels; ++lvl) {
+        const u64 qL = c->primes[lvl];
+        for (int i = 0; i <= lvl; ++i) {
+            const u64 q = c->primes[i];
+            const u64 R = r_mod(q);
+            LevelConst &L = lc[(size_t)lvl * num_rows + i];
+            const u64 pinv = invmod_h(P % q, q);
+            L.gamma = shoup_pair(pinv, q);
+            L.gamma_r = shoup_pair(mulmod_h(pinv, R, q), q);
+            L.pmod = shoup_pair(P % q, q);
+            L.pinv = shoup_pair(pinv, q);
+            if (i < lvl) {
+                const u64 qinv = invmod_h(qL % q, q);
+                L.beta = shoup_pair(qinv, q);
+                L.beta_r = shoup_pair(mulmod_h(qinv, R, q), q);
+                const u64 a = mulmod_h(pinv, qinv, q);
+                L.alpha = shoup_pair(a, q);
+                L.alpha_r = shoup_pair(mulmod_h(a, R, q), q);
+            }
+        }
+    }
+    cudaError_t e;
+    if ((e = cudaSetDevice(device)) != cudaSuccess ||
+        (e = cudaMalloc(&c->d_pi, sizeof(PrimeInfo) * num_rows)) != cudaSuccess ||
+        (e = cudaMalloc(&c->d_tw, sizeof(ulonglong2) * tw.size())) != cudaSuccess ||
+        (e = cudaMalloc(&c->d_itw, sizeof(ulonglong2) * itw.size())) != cudaSuccess ||
+        (e = cudaMalloc(&c->d_lc, sizeof(LevelConst) * lc.size())) != cudaSuccess ||
+        (e = cudaMalloc(&c->d_last, sizeof(LastConst) * num_rows)) != cudaSuccess ||
+        (e = cudaMemcpy(c->d_pi, pi.data(), sizeof(PrimeInfo) * num_rows, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(c->d_tw, tw.data(), sizeof(ulonglong2) * tw.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(c->d_itw, itw.data(), sizeof(ulonglong2) * itw.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(c->d_lc, lc.data(), sizeof(LevelConst) * lc.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(c->d_last, last.data(), sizeof(LastConst) * num_rows, cudaMemcpyHostToDevice)) != cudaSuccess) {
+        heb_ctx_destroy(c);
+        return fail(HEB_ECUDA, "context upload failed: %s", cudaGetErrorString(e));
+    }
+    *out = c;
+    return HEB_OK;
+}
+
+extern "C" int heb_ctx_destroy(heb_ctx *c) {
+    if (!c) return HEB_OK;
+    cudaFree(c->d_pi);
+    cudaFree(c->d_tw);
+    cudaFree(c->d_itw);
+    cudaFree(c->d_lc);
+    cudaFree(c->d_last);
+    delete c;
+    return HEB_OK;
+}
+
+extern "C" int heb_ctx_ring_degree(const heb_ctx *c) { return c ? c->n : 0; }
+extern "C" int heb_ctx_set_chunk(heb_ctx *c, int items) {
+    if (!c || items < 1) return fail(HEB_EINVAL, "bad chunk");
+    c->chunk = items;
+    return HEB_OK;
+}
+
+// =============================================================================
+// memory
+// =============================================================================
+extern "C" int heb_alloc(size_t bytes, void **out, void *stream) {
+    if (cudaMallocAsync(out, bytes ? bytes : 8, (cudaStream_t)stream) != cudaSuccess)
+        return fail(HEB_ENOMEM, "cudaMallocAsync(%zu) failed", bytes);
+    return HEB_OK;
+}
+extern "C" int heb_free(void *ptr, void *stream) {
+    CUDA_TRY(cudaFreeAsync(ptr, (cudaStream_t)stream));
+    return HEB_OK;
+}
+extern "C" int heb_h2d(void *dst, const void *src, size_t bytes, void *stream) {
+    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    return HEB_OK;
+}
+extern "C" int heb_d2h(void *dst, const void *src, size_t bytes, void *stream) {
+    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    return HEB_OK;
+}
+extern "C" int heb_sync(void *stream) {
+    CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    return HEB_OK;
+}
+

@@ -1,0 +1,340 @@
+// keyswitch.cu -- rescale, relinearisation (key switch + ModDown + rescale) and rotation.
+#include "common.cuh"
+
+// =============================================================================
+// rescale (divide_drop_last, kernels.py:270-294), optionally fused with ct x pt
+//   head: v = center(INTT_L(c_L [* pt_L]))                      (1 INTT / component)
+//   tail: out_i = c_i [* pt_i] * qL^-1 - NTT_i(v * qL^-1 * R)  (k-1 NTTs / component)
+// =============================================================================
+template <int LOGN>
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_rescale_head(Ctx K, heb_ct in, const u64 *pt,
+                                                                        int64_t pstride, i64 *V, int comps, int L,
+                                                                        int64_t count) {
+    extern __shared__ u64 sm[];
+    const int c = blockIdx.x;
+    const PrimeInfo P = K.pi[L];
+    const LastConst lc = K.last[L];
+    for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
+        u64 x[16];
+        load16(at(in, b, c, L, LOGN) + threadIdx.x * 16, x);
+        if (pt) {
+            u64 y[16];
+            load16(pt + b * pstride + ((int64_t)L << LOGN) + threadIdx.x * 16, y);
+#pragma unroll
+            for (int m = 0; m < 16; ++m) x[m] = mont_mul(x[m], y[m], P.p, P.pinv);
+        }
+        i64 *dst = V + (b * comps + c) * (1 << LOGN);
+        ntt::inverse<LOGN>(sm, itw_row<LOGN>(K, L), P.p, x, [&](int i, u64 v) { dst[i] = center(v, P.p); },
+                           lc.u_std, lc.v_std);
+    }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_rescale_tail(Ctx K, heb_ct in, const u64 *pt,
+                                                                        int64_t pstride, const i64 *V, heb_ct out,
+                                                                        int comps, int L, int64_t count) {
+    extern __shared__ u64 sm[];
+    const int i = blockIdx.x, c = blockIdx.z;
+    const PrimeInfo P = K.pi[i];
+    const LevelConst C = K.lc[(size_t)L * K.num_rows + i];
+    for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
+        const i64 *src = V + (b * comps + c) * (1 << LOGN);
+        u64 y[16];
+        ntt::forward<LOGN>(sm, tw_row<LOGN>(K, i), P.p,
+                           [&](int j) { return signed_mul_const(src[j], C.beta_r.x, C.beta_r.y, P.p); }, y);
+        u64 x[16];
+        load16(at(in, b, c, i, LOGN) + threadIdx.x * 16, x);
+        if (pt) {
+            u64 z[16];
+            load16(pt + b * pstride + ((int64_t)i << LOGN) + threadIdx.x * 16, z);
+#pragma unroll
+            for (int m = 0; m < 16; ++m) x[m] = mont_mul(x[m], z[m], P.p, P.pinv);
+        }
+#pragma unroll
+        for (int m = 0; m < 16; ++m) x[m] = sub_mod(shoup(x[m], C.beta.x, C.beta.y, P.p), y[m], P.p);
+        store16(at(out, b, c, i, LOGN) + threadIdx.x * 16, x);
+    }
+}
+
+template <int LOGN>
+static int launch_rescale(heb_ctx *c, heb_ct in, const u64 *pt, int64_t pstride, heb_ct out, int64_t count, int comps,
+                          int level, cudaStream_t st) {
+    constexpr int T = ntt::Shape<LOGN>::T;
+    constexpr size_t sm = smem_bytes<LOGN>();
+    CUDA_TRY(prep_kernel(k_rescale_head<LOGN>, sm));
+    CUDA_TRY(prep_kernel(k_rescale_tail<LOGN>, sm));
+    const int64_t chunk = c->chunk > 0 ? c->chunk * 4 : count;
+    Scratch V(st);
+    CUDA_TRY(V.get(sizeof(i64) * (size_t)std::min<int64_t>(count, chunk) * comps * c->n));
+    for (int64_t b0 = 0; b0 < count; b0 += chunk) {
+        const int64_t cnt = std::min<int64_t>(chunk, count - b0);
+        heb_ct ib = in, ob = out;
+        ib.data += b0 * in.ct_stride;
+        ob.data += b0 * out.ct_stride;
+        const u64 *pb = pt ? pt + b0 * pstride : nullptr;
+        k_rescale_head<LOGN><<<dim3(comps, gdim(cnt)), T, sm, st>>>(kctx(c), ib, pb, pstride, (i64 *)V.p, comps,
+                                                                     level, cnt);
+        LAUNCH_CHECK();
+        k_rescale_tail<LOGN><<<dim3(level, gdim(cnt), comps), T, sm, st>>>(kctx(c), ib, pb, pstride,
+                                                                            (const i64 *)V.p, ob, comps, level, cnt);
+        LAUNCH_CHECK();
+    }
+    return HEB_OK;
+}
+
+extern "C" int heb_rescale(heb_ctx *c, heb_ct in, const uint64_t *pt, int64_t pstride, heb_ct out, int64_t count,
+                           int comps, int level, void *stream) {
+    if (!c || level < 1 || level > c->num_rows - 2 || comps < 1) return fail(HEB_EINVAL, "heb_rescale: bad level %d", level);
+    if (count <= 0) return HEB_OK;
+    if (out.data == in.data) return fail(HEB_EINVAL, "heb_rescale: output must not alias input");
+    DISPATCH_LOGN(c, launch_rescale, c, in, pt, pstride, out, count, comps, level, (cudaStream_t)stream);
+}
+
+// =============================================================================
+// key switching (relin_accumulate + moddown_special, kernels.py:297-371) and the
+// fused ModDown + rescale of raw_finalize (ckks.py:359-387).
+//   head : D_j = center(INTT_j(d2_j))                                     k INTT
+//   modup: acc_t = sum_j NTT_t(D_j mod p_t) (*) key[j][t]  (t<k and P)      k^2 NTT
+//   ModDown+rescale per component c (q_L = row k-1, P = special):
+//     aP = center(INTT_P(acc_P));  bL = INTT_L(acc_L + P d_L)              2 INTT
+//     sL = (bL - aP) P^-1 mod q_L ; cL = center(sL)
+//     out_i = acc_i P^-1 qL^-1 + d_i qL^-1 - NTT_i(aP P^-1 qL^-1 R + cL qL^-1 R)
+//                                                                       k-1 NTT
+// which equals moddown -> add d -> divide_drop_last of the reference exactly,
+// since every step is an identity mod q_i.
+// =============================================================================
+template <int LOGN>
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_ks_head(Ctx K, heb_ct src, int comp, i64 *D, int k,
+                                                                   int64_t count) {
+    extern __shared__ u64 sm[];
+    const int j = blockIdx.x;
+    const PrimeInfo P = K.pi[j];
+    const LastConst lc = K.last[j];
+    for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
+        u64 x[16];
+        load16(at(src, b, comp, j, LOGN) + threadIdx.x * 16, x);
+        i64 *dst = D + (b * k + j) * (1 << LOGN);
+        ntt::inverse<LOGN>(sm, itw_row<LOGN>(K, j), P.p, x, [&](int i, u64 v) { dst[i] = center(v, P.p); },
+                           lc.u_std, lc.v_std);
+    }
+}
+
+// acc layout: (count, 2, k+1, N); row k is the special prime
+template <int LOGN>
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_ks_modup(Ctx K, heb_ct src, int comp, const i64 *D,
+                                                                    const u64 *kb, const u64 *ka, int k,
+                                                                    u64 *acc, int64_t count) {
+    extern __shared__ u64 sm[];
+    const int t = blockIdx.x;
+    const int gt = t < k ? t : K.num_rows - 1;
+    const PrimeInfo P = K.pi[gt];
+    const int n = 1 << LOGN;
+    const int pos = threadIdx.x * 16;
+    for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
+        u64 a0[16], a1[16];
+#pragma unroll
+        for (int m = 0; m < 16; ++m) a0[m] = a1[m] = 0;
+        for (int j = 0; j < k; ++j) {
+            u64 dig[16];
+            if (j == t) {
+                load16(at(src, b, comp, j, LOGN) + pos, dig);
+            } else {
+                const i64 *dj = D + (b * k + j) * n;
+                ntt::forward<LOGN>(sm, tw_row<LOGN>(K, gt), P.p,
+                                   [&](int i) { return signed_mul_const(dj[i], P.rmod, P.rmod_s, P.p); }, dig);
+            }
+            const size_t koff = ((size_t)j * K.num_rows + gt) * n + pos;
+            u64 eb[16], ea[16];
+            load16(kb + koff, eb);
+            load16(ka + koff, ea);
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                a0[m] = add_mod(a0[m], mont_mul(dig[m], eb[m], P.p, P.pinv), P.p);
+                a1[m] = add_mod(a1[m], mont_mul(dig[m], ea[m], P.p, P.pinv), P.p);
+            }
+        }
+        u64 *o0 = acc + ((b * 2 + 0) * (k + 1) + t) * n + pos;
+        u64 *o1 = acc + ((b * 2 + 1) * (k + 1) + t) * n + pos;
+        store16(o0, a0);
+        store16(o1, a1);
+    }
+}
+
+// which = 0: aP = center_P(INTT_P(acc_P)) ; which = 1: bL = INTT_L(acc_L + P d_L) (std form)
+template <int LOGN>
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_ks_down_head(Ctx K, const u64 *acc, heb_ct d, int k,
+                                                                        i64 *aP, u64 *bL, int64_t count) {
+    extern __shared__ u64 sm[];
+    const int which = blockIdx.x, c = blockIdx.z;
+    const int n = 1 << LOGN;
+    const int pos = threadIdx.x * 16;
+    const int row = which == 0 ? K.num_rows - 1 : k - 1;
+    const int arow = which == 0 ? k : k - 1;
+    const PrimeInfo P = K.pi[row];
+    const LastConst lc = K.last[row];
+    const LevelConst C = K.lc[(size_t)(k - 1) * K.num_rows + (k - 1)];
+    for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
+        u64 x[16];
+        load16(acc + ((b * 2 + c) * (k + 1) + arow) * n + pos, x);
+        if (which == 1) {
+            u64 y[16];
+            load16(at(d, b, c, k - 1, LOGN) + pos, y);
+#pragma unroll
+            for (int m = 0; m < 16; ++m) x[m] = add_mod(x[m], shoup(y[m], C.pmod.x, C.pmod.y, P.p), P.p);
+            u64 *dst = bL + (b * 2 + c) * n;
+            ntt::inverse<LOGN>(sm, itw_row<LOGN>(K, row), P.p, x, [&](int i, u64 v) { dst[i] = v; }, lc.u_std,
+                               lc.v_std);
+        } else {
+            i64 *dst = aP + (b * 2 + c) * n;
+            ntt::inverse<LOGN>(sm, itw_row<LOGN>(K, row), P.p, x, [&](int i, u64 v) { dst[i] = center(v, P.p); },
+                               lc.u_std, lc.v_std);
+        }
+    }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_ks_down_rescale_tail(Ctx K, const u64 *acc, heb_ct d,
+                                                                                const i64 *aP, const u64 *bL, int k,
+                                                                                heb_ct out, int64_t count) {
+    extern __shared__ u64 sm[];
+    const int i = blockIdx.x, c = blockIdx.z;
+    const int n = 1 << LOGN;
+    const int pos = threadIdx.x * 16;
+    const int L = k - 1;
+    const PrimeInfo Pi = K.pi[i];
+    const PrimeInfo PL = K.pi[L];
+    const LevelConst Ci = K.lc[(size_t)L * K.num_rows + i];  // level L: drop q_L
+    const LevelConst CL = K.lc[(size_t)L * K.num_rows + L];  // P^-1 mod q_L
+    for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
+        const i64 *ap = aP + (b * 2 + c) * n;
+        const u64 *bl = bL + (b * 2 + c) * n;
+        u64 y[16];
+        ntt::forward<LOGN>(
+            sm, tw_row<LOGN>(K, i), Pi.p,
+            [&](int j) {
+                const i64 a = ap[j];
+                // s_L = (bL - aP) * P^-1 mod q_L, centred
+                const u64 sl = sub_mod(shoup(bl[j], CL.pinv.x, CL.pinv.y, PL.p),
+                                       signed_mul_const(a, CL.pinv.x, CL.pinv.y, PL.p), PL.p);
+                const i64 cl = center(sl, PL.p);
+                return add_mod(signed_mul_const(a, Ci.alpha_r.x, Ci.alpha_r.y, Pi.p),
+                               signed_mul_const(cl, Ci.beta_r.x, Ci.beta_r.y, Pi.p), Pi.p);
+            },
+            y);
+        u64 x[16], z[16];
+        load16(acc + ((b * 2 + c) * (k + 1) + i) * n + pos, x);
+        load16(at(d, b, c, i, LOGN) + pos, z);
+#pragma unroll
+        for (int m = 0; m < 16; ++m)
+            x[m] = sub_mod(add_mod(shoup(x[m], Ci.alpha.x, Ci.alpha.y, Pi.p), shoup(z[m], Ci.beta.x, Ci.beta.y, Pi.p),
+                                   Pi.p),
+                           y[m], Pi.p);
+        store16(at(out, b, c, i, LOGN) + pos, x);
+    }
+}
+
+// ModDown without rescale (rotation): out_i = acc_i P^-1 - NTT_i(aP P^-1 R) [+ add0_i for c = 0]
+template <int LOGN>
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_ks_down_tail(Ctx K, const u64 *acc, const i64 *aP, int k,
+                                                                        heb_ct add0, heb_ct out, int64_t count) {
+    extern __shared__ u64 sm[];
+    const int i = blockIdx.x, c = blockIdx.z;
+    const int n = 1 << LOGN;
+    const int pos = threadIdx.x * 16;
+    const PrimeInfo Pi = K.pi[i];
+    const LevelConst Ci = K.lc[(size_t)(k - 1) * K.num_rows + i];
+    for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
+        const i64 *ap = aP + (b * 2 + c) * n;
+        u64 y[16];
+        ntt::forward<LOGN>(sm, tw_row<LOGN>(K, i), Pi.p,
+                           [&](int j) { return signed_mul_const(ap[j], Ci.gamma_r.x, Ci.gamma_r.y, Pi.p); }, y);
+        u64 x[16];
+        load16(acc + ((b * 2 + c) * (k + 1) + i) * n + pos, x);
+#pragma unroll
+        for (int m = 0; m < 16; ++m) x[m] = sub_mod(shoup(x[m], Ci.gamma.x, Ci.gamma.y, Pi.p), y[m], Pi.p);
+        if (c == 0) {
+            u64 z[16];
+            load16(at(add0, b, 0, i, LOGN) + pos, z);
+#pragma unroll
+            for (int m = 0; m < 16; ++m) x[m] = add_mod(x[m], z[m], Pi.p);
+        }
+        store16(at(out, b, c, i, LOGN) + pos, x);
+    }
+}
+
+template <int LOGN>
+static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const u64 *kb, const u64 *ka, heb_ct d, heb_ct out,
+                            int64_t count, int level, bool rescale, cudaStream_t st) {
+    constexpr int T = ntt::Shape<LOGN>::T;
+    constexpr size_t sm = smem_bytes<LOGN>();
+    CUDA_TRY(prep_kernel(k_ks_head<LOGN>, sm));
+    CUDA_TRY(prep_kernel(k_ks_modup<LOGN>, sm));
+    CUDA_TRY(prep_kernel(k_ks_down_head<LOGN>, sm));
+    CUDA_TRY(prep_kernel(k_ks_down_rescale_tail<LOGN>, sm));
+    CUDA_TRY(prep_kernel(k_ks_down_tail<LOGN>, sm));
+    const int k = level + 1, n = c->n;
+    const int64_t chunk = c->chunk > 0 ? c->chunk : count;
+    const int64_t cmax = std::min<int64_t>(chunk, count);
+    Scratch sD(st), sA(st), sP(st), sL(st);
+    CUDA_TRY(sD.get(sizeof(i64) * (size_t)cmax * k * n));
+    CUDA_TRY(sA.get(sizeof(u64) * (size_t)cmax * 2 * (k + 1) * n));
+    CUDA_TRY(sP.get(sizeof(i64) * (size_t)cmax * 2 * n));
+    CUDA_TRY(sL.get(sizeof(u64) * (size_t)cmax * 2 * n));
+    const Ctx K = kctx(c);
+    for (int64_t b0 = 0; b0 < count; b0 += chunk) {
+        const int64_t cnt = std::min<int64_t>(chunk, count - b0);
+        heb_ct s = src, dd = d, o = out;
+        s.data += b0 * src.ct_stride;
+        dd.data += b0 * d.ct_stride;
+        o.data += b0 * out.ct_stride;
+        const unsigned gy = gdim(cnt);
+        k_ks_head<LOGN><<<dim3(k, gy), T, sm, st>>>(K, s, comp, (i64 *)sD.p, k, cnt);
+        LAUNCH_CHECK();
+        k_ks_modup<LOGN><<<dim3(k + 1, gy), T, sm, st>>>(K, s, comp, (const i64 *)sD.p, kb, ka, k, (u64 *)sA.p, cnt);
+        LAUNCH_CHECK();
+        if (rescale) {
+            k_ks_down_head<LOGN><<<dim3(2, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
+                                                                 (u64 *)sL.p, cnt);
+            LAUNCH_CHECK();
+            k_ks_down_rescale_tail<LOGN><<<dim3(k - 1, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, dd,
+                                                                             (const i64 *)sP.p, (const u64 *)sL.p, k,
+                                                                             o, cnt);
+            LAUNCH_CHECK();
+        } else {
+            k_ks_down_head<LOGN><<<dim3(1, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
+                                                                 (u64 *)sL.p, cnt);
+            LAUNCH_CHECK();
+            k_ks_down_tail<LOGN><<<dim3(k, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, (const i64 *)sP.p, k, dd, o,
+                                                                 cnt);
+            LAUNCH_CHECK();
+        }
+    }
+    return HEB_OK;
+}
+
+extern "C" int heb_relin_rescale(heb_ctx *c, heb_ct raw, const uint64_t *evk_b, const uint64_t *evk_a, heb_ct out,
+                                 int64_t count, int level, void *stream) {
+    if (!c || !evk_b || !evk_a || level < 1 || level > c->num_rows - 2)
+        return fail(HEB_EINVAL, "heb_relin_rescale: bad level %d", level);
+    if (count <= 0) return HEB_OK;
+    // d2 = component 2 of raw; d0/d1 = components 0/1
+    DISPATCH_LOGN(c, launch_keyswitch, c, raw, 2, evk_b, evk_a, raw, out, count, level, true, (cudaStream_t)stream);
+}
+
+extern "C" int heb_rotate(heb_ctx *c, heb_ct ct, const uint64_t *gk_b, const uint64_t *gk_a, heb_ct out,
+                          int64_t count, int level, uint64_t galois, void *stream) {
+    if (!c || !gk_b || !gk_a || level < 0 || level > c->num_rows - 2 || !(galois & 1))
+        return fail(HEB_EINVAL, "heb_rotate: bad args");
+    if (count <= 0) return HEB_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int k = level + 1;
+    // sigma_g of both components into a compact scratch batch
+    Scratch rot(st);
+    CUDA_TRY(rot.get(sizeof(u64) * (size_t)count * 2 * k * c->n));
+    heb_ct r{(u64 *)rot.p, (int64_t)2 * k * c->n, (int64_t)k * c->n};
+    const int64_t lines = count * 2 * k;
+    k_galois_ct<<<pw_grid(c->n, lines), 256, 0, st>>>(ct, r, lines, k, c->log_n, galois % (2ull * c->n));
+    LAUNCH_CHECK();
+    DISPATCH_LOGN(c, launch_keyswitch, c, r, 1, gk_b, gk_a, r, out, count, level, false, st);
+}
+

@@ -1,0 +1,201 @@
+// ntt.cuh -- CTA-cooperative negacyclic NTT engine for sm_100a.
+//
+// Transform (reference kernels.py:68-114):
+//   forward: natural-order input, output position i holds a(psi^(2*brv(i)+1));
+//            Cooley-Tukey stages s = 0..n-1, stage s pairs (j, j + N/2^(s+1)) inside
+//            block b = j >> (n-s) with twiddle tw[2^s + b] = psi^brv(2^s + b);
+//   inverse: the exact inverse map (Gentleman-Sande with tw^-1, stages n-1..0, times
+//            n^-1 folded into the last stage), so results are bit-identical to the
+//            reference's backwards table walk.
+//
+// Work split: one CTA of T = N/16 threads owns one row of N residues.  The n stages
+// are processed in register-blocked groups: a radix-2^r group gives each thread a
+// "unit" of 2^r elements that stay in registers for r stages; units exchange through
+// shared memory between groups (padded index i + i/16 keeps 64-bit accesses free of
+// bank conflicts for every group shape used here).  n = 4*G + REM gives G radix-16
+// groups plus one radix-2^REM group (first in forward order, last in inverse order).
+//
+// Interfaces chosen so that callers can fuse prologues/epilogues:
+//   forward: input through a functor load(idx) (coalesced across threads), output
+//            left in registers: thread t holds positions [16t, 16t+16) of the result;
+//   inverse: input given in registers in that same layout, output through a functor
+//            store(idx, value) (coalesced).
+// Lazy reduction: forward values live in [0, 4p), inverse values in [0, 2p); all
+// values handed to the caller are canonical.
+#pragma once
+#include "modarith.cuh"
+
+namespace ntt {
+
+HD int pad(int i) { return i + (i >> 4); }
+
+template <int LOGN>
+struct Shape {
+    static constexpr int N = 1 << LOGN;
+    static constexpr int T = N / 16;
+    static constexpr int REM = LOGN % 4;
+    static constexpr int G = LOGN / 4;
+    static constexpr int SMEM_WORDS = N + N / 16;
+};
+
+// ---------------------------------------------------------------- forward ----
+// One forward group: radix 2^RB covering stages S0 .. S0+RB-1.
+// SRC: 0 = functor load, 1 = shared memory.  DST: 0 = shared memory, 1 = registers.
+template <int LOGN, int RB, int S0, int SRC, int DST, class Load>
+HD void fwd_group(u64 *sm, const ulonglong2 *__restrict__ tw, u64 p, Load &load, u64 (&out)[16]) {
+    using S = Shape<LOGN>;
+    constexpr int R = 1 << RB;
+    constexpr int LB = LOGN - S0 - RB;
+    constexpr int UPT = (S::N / R) / S::T;
+    const u64 p2 = 2 * p;
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < UPT; ++k) {
+        const int u = tid + k * S::T;
+        const int ulow = u & ((1 << LB) - 1);
+        const int uhigh = u >> LB;
+        const int base = (uhigh << (LOGN - S0)) | ulow;
+        u64 x[R];
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            const int idx = base + (m << LB);
+            if constexpr (SRC == 0) x[m] = load(idx);
+            else x[m] = sm[pad(idx)];
+        }
+#pragma unroll
+        for (int q = 0; q < RB; ++q) {
+            const int half = R >> (q + 1);
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                if (m & half) continue;
+                const ulonglong2 w = tw[(1 << (S0 + q)) + (uhigh << q) + (m >> (RB - q))];
+                u64 a = csub(x[m], p2);
+                u64 t = shoup_lazy(x[m + half], w.x, w.y, p);
+                x[m] = a + t;
+                x[m + half] = a - t + p2;
+            }
+        }
+        if constexpr (DST == 1) {
+            static_assert(UPT == 1 && R == 16, "register output needs one radix-16 unit per thread");
+#pragma unroll
+            for (int m = 0; m < R; ++m) out[m] = csub(csub(x[m], p2), p);
+        } else {
+#pragma unroll
+            for (int m = 0; m < R; ++m) sm[pad(base + (m << LB))] = x[m];
+        }
+    }
+}
+
+template <int LOGN, int GI, class Load>
+HD void fwd_radix16_groups(u64 *sm, const ulonglong2 *__restrict__ tw, u64 p, Load &load, u64 (&out)[16]) {
+    using S = Shape<LOGN>;
+    constexpr int S0 = S::REM + 4 * GI;
+    constexpr bool first = (S0 == 0);
+    constexpr bool last = (GI == S::G - 1);
+    fwd_group<LOGN, 4, S0, first ? 0 : 1, last ? 1 : 0>(sm, tw, p, load, out);
+    if constexpr (!last) {
+        __syncthreads();
+        fwd_radix16_groups<LOGN, GI + 1>(sm, tw, p, load, out);
+    }
+}
+
+// Forward NTT of one row.  `load(idx)` returns the input residue at natural position
+// idx (in [0, 2p)); on return thread t holds output positions 16t .. 16t+15.
+template <int LOGN, class Load>
+__device__ void forward(u64 *sm, const ulonglong2 *__restrict__ tw, u64 p, Load load, u64 (&out)[16]) {
+    using S = Shape<LOGN>;
+    static_assert(LOGN >= 6 && LOGN <= 14, "single-CTA engine covers N = 64 .. 16384");
+    __syncthreads();  // shared memory may still be read by a previous transform
+    if constexpr (S::REM) {
+        fwd_group<LOGN, S::REM, 0, 0, 0>(sm, tw, p, load, out);
+        __syncthreads();
+    }
+    fwd_radix16_groups<LOGN, 0>(sm, tw, p, load, out);
+}
+
+// ---------------------------------------------------------------- inverse ----
+// SRC: 1 = registers, 0 = shared memory.  DST: 0 = shared memory, 1 = functor store.
+template <int LOGN, int RB, int S0, int SRC, int DST, class Store>
+HD void inv_group(u64 *sm, const ulonglong2 *__restrict__ itw, u64 p, const u64 (&in)[16], Store &store,
+                  ulonglong2 last_u, ulonglong2 last_v) {
+    using S = Shape<LOGN>;
+    constexpr int R = 1 << RB;
+    constexpr int LB = LOGN - S0 - RB;
+    constexpr int UPT = (S::N / R) / S::T;
+    const u64 p2 = 2 * p;
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < UPT; ++k) {
+        const int u = tid + k * S::T;
+        const int ulow = u & ((1 << LB) - 1);
+        const int uhigh = u >> LB;
+        const int base = (uhigh << (LOGN - S0)) | ulow;
+        u64 x[R];
+        if constexpr (SRC == 1) {
+            static_assert(UPT == 1 && R == 16, "register input needs one radix-16 unit per thread");
+#pragma unroll
+            for (int m = 0; m < R; ++m) x[m] = in[m];
+        } else {
+#pragma unroll
+            for (int m = 0; m < R; ++m) x[m] = sm[pad(base + (m << LB))];
+        }
+#pragma unroll
+        for (int q = RB - 1; q >= 0; --q) {
+            const int half = R >> (q + 1);
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                if (m & half) continue;
+                const u64 a = x[m], b = x[m + half];
+                if (S0 + q == 0) {
+                    // final stage: fold n^-1 (and optionally R^-1) and canonicalise
+                    x[m] = shoup(a + b, last_u.x, last_u.y, p);
+                    x[m + half] = shoup(a - b + p2, last_v.x, last_v.y, p);
+                } else {
+                    const ulonglong2 w = itw[(1 << (S0 + q)) + (uhigh << q) + (m >> (RB - q))];
+                    x[m] = csub(a + b, p2);
+                    x[m + half] = shoup_lazy(a - b + p2, w.x, w.y, p);
+                }
+            }
+        }
+        if constexpr (DST == 1) {
+#pragma unroll
+            for (int m = 0; m < R; ++m) store(base + (m << LB), x[m]);
+        } else {
+#pragma unroll
+            for (int m = 0; m < R; ++m) sm[pad(base + (m << LB))] = x[m];
+        }
+    }
+}
+
+template <int LOGN, int GI, class Store>
+HD void inv_radix16_groups(u64 *sm, const ulonglong2 *__restrict__ itw, u64 p, const u64 (&in)[16], Store &store,
+                           ulonglong2 last_u, ulonglong2 last_v) {
+    // GI counts down from G-1 (first inverse group, register input) to 0.
+    using S = Shape<LOGN>;
+    constexpr int S0 = S::REM + 4 * GI;
+    constexpr bool first = (GI == S::G - 1);
+    constexpr bool last = (S0 == 0);
+    inv_group<LOGN, 4, S0, first ? 1 : 0, last ? 1 : 0>(sm, itw, p, in, store, last_u, last_v);
+    if constexpr (GI > 0) {
+        __syncthreads();
+        inv_radix16_groups<LOGN, GI - 1>(sm, itw, p, in, store, last_u, last_v);
+    }
+}
+
+// Inverse NTT of one row.  Thread t supplies positions 16t .. 16t+15 (values in
+// [0, 2p)); results leave through store(idx, canonical value).  last_u = n^-1 * c and
+// last_v = itw[1] * n^-1 * c (Shoup pairs) for a caller-chosen output factor c.
+template <int LOGN, class Store>
+__device__ void inverse(u64 *sm, const ulonglong2 *__restrict__ itw, u64 p, const u64 (&in)[16], Store store,
+                        ulonglong2 last_u, ulonglong2 last_v) {
+    using S = Shape<LOGN>;
+    static_assert(LOGN >= 6 && LOGN <= 14, "single-CTA engine covers N = 64 .. 16384");
+    __syncthreads();
+    inv_radix16_groups<LOGN, S::G - 1>(sm, itw, p, in, store, last_u, last_v);
+    if constexpr (S::REM) {
+        __syncthreads();
+        inv_group<LOGN, S::REM, 0, 0, 1>(sm, itw, p, in, store, last_u, last_v);
+    }
+}
+
+}  // namespace ntt

@@ -1,0 +1,195 @@
+"""Bit-exact parity of the CUDA product path against the CPU oracle and the
+reference's golden vectors.  Needs a B200 (marked gpu)."""
+
+import hashlib
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from conftest import S128, s128_params
+
+pytestmark = pytest.mark.gpu
+
+
+def digest(arr):
+    return hashlib.sha256(np.ascontiguousarray(arr).astype("<u8").tobytes()).hexdigest()
+
+
+def frac(s):
+    a, b = s.split("/")
+    return Fraction(int(a), int(b))
+
+
+@pytest.fixture(scope="module")
+def dev_s128():
+    from paper_2102_00319_b200.backend import B200Backend
+
+    be = B200Backend(s128_params(), S128["extra"])
+    keys = be.keygen(galois_steps=(1,))
+    be.set_eval_key(keys)
+    return be, keys
+
+
+def host(be, ct):
+    c0, c1 = be.cipher_rows_host(ct)
+    return c0, c1
+
+
+def test_ntt_pair_matches_reference(s128):
+    import torch
+    from paper_2102_00319_b200.backend import DeviceContext, u64_to_dev, dev_to_u64
+    from paper_2102_00319_b200.chain import build_chain
+
+    ctx = DeviceContext(build_chain(s128_params(), S128["extra"]))
+    rows = s128["ntt_in"].shape[0]
+    d = u64_to_dev(s128["ntt_in"], ctx.device)
+    ctx.call("heb_ntt_fwd", d.data_ptr(), 1, rows, 0, rows * ctx.n, ctx.stream)
+    assert np.array_equal(dev_to_u64(d), s128["ntt_fwd"])
+    ctx.call("heb_ntt_inv", d.data_ptr(), 1, rows, 0, rows * ctx.n, ctx.stream)
+    assert np.array_equal(dev_to_u64(d), s128["ntt_in"])
+    d = u64_to_dev(s128["ntt_in"], ctx.device)
+    ctx.call("heb_ntt_inv", d.data_ptr(), 1, rows, 0, rows * ctx.n, ctx.stream)
+    assert np.array_equal(dev_to_u64(d), s128["ntt_inv"])
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("logn", [6, 8, 10, 12, 13, 14])
+def test_ntt_matches_oracle_all_sizes(logn):
+    from oracle import ckks_oracle as oc
+    from paper_2102_00319_b200.backend import DeviceContext, u64_to_dev, dev_to_u64
+    from paper_2102_00319_b200.chain import build_chain
+    from paper_2102_00319_b200.params import derive_params
+
+    n = 1 << logn
+    ch = build_chain(derive_params(2 * n, 200, 40, seed=1), 20)
+    ctx = DeviceContext(ch)
+    rng = np.random.default_rng(logn)
+    rows = ch.num_rows
+    x = np.stack([rng.integers(0, int(q), n, dtype=np.uint64) for q in ch.p])
+    ref = x.copy()
+    oc.ntt_fwd_rows(ref, ch.twiddles, ch.p, ch.p_inv)
+    d = u64_to_dev(np.stack([x, x]), ctx.device)
+    ctx.call("heb_ntt_fwd", d.data_ptr(), 2, rows, 0, rows * n, ctx.stream)
+    got = dev_to_u64(d)
+    assert np.array_equal(got[0], ref) and np.array_equal(got[1], ref)
+    ctx.call("heb_ntt_inv", d.data_ptr(), 2, rows, 0, rows * n, ctx.stream)
+    assert np.array_equal(dev_to_u64(d)[1], x)
+
+
+class TestS128:
+    def test_keys_bit_exact(self, s128, dev_s128):
+        from paper_2102_00319_b200.backend import dev_to_u64
+
+        _, keys = dev_s128
+        assert np.array_equal(dev_to_u64(keys.secret.s_eval), s128["s_eval"])
+        assert np.array_equal(dev_to_u64(keys.public.b), s128["pk_b"])
+        assert np.array_equal(dev_to_u64(keys.public.a), s128["pk_a"])
+        assert np.array_equal(dev_to_u64(keys.evaluation.b), s128["evk_b"])
+        assert np.array_equal(dev_to_u64(keys.evaluation.a), s128["evk_a"])
+
+    def test_ops_bit_exact(self, s128, dev_s128, golden):
+        be, keys = dev_s128
+        a = be.encrypt(s128["va"], keys, entropy=1)
+        b = be.encrypt(s128["vb"], keys, entropy=2)
+
+        def same(name, ct):
+            c0, c1 = host(be, ct)
+            assert np.array_equal(c0, s128[f"{name}_c0"]), name
+            assert np.array_equal(c1, s128[f"{name}_c1"]), name
+
+        same("a", a)
+        same("b", b)
+        raw = be.mul_ct_ct_raw(a, b)
+        from paper_2102_00319_b200.backend import dev_to_u64
+
+        rh = dev_to_u64(raw.payload.buf)
+        for i in range(3):
+            assert np.array_equal(rh[i], s128[f"raw_d{i}"]), i
+        fin = be.raw_finalize(be.raw_add(raw, be.mul_ct_ct_raw(a, a)))
+        same("fin", fin)
+        assert fin.scale == frac(golden["s128"]["fin"]["scale"])
+        assert np.array_equal(be.decrypt(fin, keys).values, s128["fin_dec"])
+        pt = be.encode_plain(s128["vb"], level=a.level)
+        assert np.array_equal(dev_to_u64(pt.payload.rows), s128["pt_rows"])
+        same("ctpt", be.mul_ct_pt(a, pt))
+        same("add", be.add_ct_ct(a, b))
+        same("addpt", be.add_ct_pt(a, s128["vb"]))
+        same("drop_mul", be.mul_ct_ct(be.drop_to_level(a, 3), b))
+
+    def test_rescale_every_level(self, s128, dev_s128):
+        from paper_2102_00319_b200.backend import u64_to_dev, dev_to_u64, ct_desc
+
+        be, _ = dev_s128
+        for lvl in range(1, be.fresh_level + 1):
+            comp = s128[f"resc_in_{lvl}"]
+            d = u64_to_dev(comp[None], be.dev)  # (1 comp, k, n)
+            out = be.ctx.empty(1, lvl, be.n)
+            be.ctx.call("heb_rescale", ct_desc(d), None, 0, ct_desc(out), 1, 1, lvl, be.ctx.stream)
+            assert np.array_equal(dev_to_u64(out)[0], s128[f"resc_out_{lvl}"]), lvl
+
+    def test_square_chain(self, s128, dev_s128, golden):
+        be, keys = dev_s128
+        ct = be.encrypt(np.full(be.slots, 1.01), keys, entropy=3)
+        for step, rec in enumerate(golden["s128"]["square_trace"]):
+            ct = be.mul_ct_ct(ct, ct)
+            c0, c1 = host(be, ct)
+            assert np.array_equal(c0, s128[f"sq{step}_c0"]) and np.array_equal(c1, s128[f"sq{step}_c1"]), step
+            assert ct.level == rec["level"] and ct.scale == frac(rec["scale"])
+
+    def test_rotation_matches_oracle(self, dev_s128, oracle_s128):
+        be, keys = dev_s128
+        ob, okeys = oracle_s128
+        v = np.random.default_rng(4).uniform(-1, 1, be.slots)
+        ct = be.encrypt(v, keys, entropy=9)
+        oct_ = ob.encrypt(v, okeys, entropy=9)
+        r = be.rotate(ct, 1)
+        orr = ob.rotate(oct_, 1)
+        c0, c1 = host(be, r)
+        assert np.array_equal(c0, orr.payload.c0) and np.array_equal(c1, orr.payload.c1)
+        lvl2 = be.rotate(be.drop_to_level(ct, 2), 1)
+        olvl2 = ob.rotate(ob.drop_to_level(oct_, 2), 1)
+        assert np.array_equal(host(be, lvl2)[0], olvl2.payload.c0)
+
+    @pytest.mark.parametrize("name", ["mini2", "mini3", "mini4"])
+    def test_mini_cnn_percell_matches_reference(self, golden, dev_s128, name):
+        from nets import mini_networks
+        from paper_2102_00319_b200 import percell
+
+        be, keys = dev_s128
+        net = mini_networks()[name]
+        imgs = np.random.default_rng(13).uniform(0, 1, (be.slots, 12, 12))[:, : net.input_dims[0], : net.input_dims[1]]
+        be.counters.reset()
+        enc = percell.encrypt_network(be, net, keys)
+        grid = percell.encrypt_images(be, imgs, keys)
+        logits = percell.run_network(be, enc, grid)
+        g = golden["minis"][name]
+        assert [digest(np.concatenate(host(be, c))) for c in logits] == g["logit_digests"]
+        assert be.counters.snapshot().__dict__ == g["counters"]
+
+
+def test_cfg1_digests_match_reference(golden):
+    from paper_2102_00319_b200.backend import B200Backend, dev_to_u64
+    from paper_2102_00319_b200.configs import CONFIGS
+
+    cfg = CONFIGS["cfg1"]
+    be = B200Backend(cfg.params(), cfg.base_extra_bits)
+    keys = be.keygen()
+    be.set_eval_key(keys)
+    g = golden["cfg1_ops"]
+    assert digest(dev_to_u64(keys.secret.s_eval)) == g["s_eval"]
+    assert digest(np.concatenate([dev_to_u64(keys.public.b), dev_to_u64(keys.public.a)])) == g["pk"]
+    assert digest(np.concatenate([dev_to_u64(keys.evaluation.b).ravel(), dev_to_u64(keys.evaluation.a).ravel()])) == g["evk"]
+    rng = np.random.default_rng(101)
+    xs = rng.uniform(-1, 1, (4, be.slots))
+    ys = rng.uniform(-1, 1, (4, be.slots))
+    cd = lambda ct: digest(np.concatenate(be.cipher_rows_host(ct)))  # noqa: E731
+    for i, rec in enumerate(g["ops"]):
+        x = be.encrypt(xs[i], keys, entropy=i)
+        y = be.encrypt(ys[i], keys, entropy=256 + i)
+        assert cd(x) == rec["x"] and cd(y) == rec["y"]
+        mul = be.mul_ct_ct(x, y)
+        assert cd(mul) == rec["mul"]
+        assert cd(be.mul_ct_pt(x, be.encode_plain(ys[i], level=x.level))) == rec["ctpt"]
+        assert cd(be.add_ct_ct(x, y)) == rec["add"]
+        assert list(be.decrypt(mul, keys).values[:8]) == rec["mul_dec8"]
