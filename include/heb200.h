@@ -73,8 +73,8 @@ int heb_ntt_fwd(heb_ctx *ctx, uint64_t *data, int64_t count, int rows, int row0,
 int heb_ntt_inv(heb_ctx *ctx, uint64_t *data, int64_t count, int rows, int row0, int64_t block_stride,
                 void *stream);
 /* Centered int64 coefficients (count, N) -> evaluation rows 0..rows-1 (Montgomery).
- * Restates spread_centered + ntt_fwd_rows (ckks.py:120-126). If `all_with_special`
- * is nonzero, the row set is every chain row (keygen, ckks.py:128-129). */
+ * Restates spread_centered + ntt_fwd_rows (ckks.py:120-126); rows = num_rows gives
+ * every chain row including the special prime (keygen, ckks.py:128-129). */
 int heb_spread_ntt(heb_ctx *ctx, const int64_t *coeffs, int64_t count, uint64_t *out, int rows,
                    int64_t out_stride, void *stream);
 
@@ -139,6 +139,18 @@ int heb_sum_gather(heb_ctx *ctx, heb_ct a, const int32_t *idx, int terms, heb_ct
 /* out_o = A[idx[o]] (gather copy of k rows x comps). */
 int heb_gather(heb_ctx *ctx, heb_ct a, const int32_t *idx, heb_ct out, int64_t n_out, int comps, int k,
                void *stream);
+
+/* --- instrumentation ---------------------------------------------------------------- */
+/* Enable (1) / disable (0) per-kernel CUDA-event timing; enabling clears old records. */
+int heb_prof_enable(int on);
+/* Writes "kernel launches total_ms total_algorithmic_bytes" lines into buf; returns the
+ * full text length. */
+int heb_prof_summary(char *buf, size_t len);
+/* Override the algorithmic byte count recorded for the next profiled launch on this
+ * thread (callers that know operand reuse, e.g. convolution windows). */
+int heb_prof_next_bytes(double bytes);
+/* Shoup 64-bit modmul throughput microbenchmark (blocks*threads*iters*8 modmuls). */
+int heb_bench_modmul(int blocks, int threads, int iters, uint64_t p, double *ms_out, void *stream);
 
 #ifdef __cplusplus
 }

@@ -59,6 +59,10 @@ SIGNATURES: dict[str, list] = {
     "heb_dot_tensor": [_P, _CT, _CT, _P, _P, _I, _CT, _L, _I, _P],
     "heb_sum_gather": [_P, _CT, _P, _I, _CT, _L, _I, _I, _P],
     "heb_gather": [_P, _CT, _P, _CT, _L, _I, _I, _P],
+    "heb_prof_enable": [_I],
+    "heb_prof_summary": [ctypes.c_char_p, ctypes.c_size_t],
+    "heb_prof_next_bytes": [ctypes.c_double],
+    "heb_bench_modmul": [_I, _I, _I, _U, ctypes.POINTER(ctypes.c_double), _P],
 }
 _RET = {"heb_last_error": ctypes.c_char_p, "heb_version": ctypes.c_int, "heb_ctx_ring_degree": ctypes.c_int}
 
@@ -100,3 +104,32 @@ def check(status: int, what: str = "") -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(lib(), name)(*args), name)
+
+
+PROF_ON = False
+
+
+def prof_enable(on: bool) -> None:
+    global PROF_ON
+    lib().heb_prof_enable(1 if on else 0)
+    PROF_ON = bool(on)
+
+
+def prof_next_bytes(nbytes: float) -> None:
+    """Declare the algorithmic bytes of the next launch (only while profiling)."""
+    if PROF_ON:
+        lib().heb_prof_next_bytes(float(nbytes))
+
+
+def prof_summary() -> dict[str, tuple[int, float, float]]:
+    """{kernel: (launches, total_ms, algorithmic_bytes)} since prof_enable(True)."""
+    size = lib().heb_prof_summary(None, 0)
+    if size < 0:
+        check(size, "heb_prof_summary")
+    buf = ctypes.create_string_buffer(size + 1)
+    lib().heb_prof_summary(buf, size + 1)
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms, nbytes = line.split()
+        out[name] = (int(cnt), float(ms), float(nbytes))
+    return out

@@ -27,6 +27,27 @@ int fail(int code, const char *fmt, ...);
 
 #define LAUNCH_CHECK() CUDA_TRY(cudaGetLastError())
 
+// Optional per-kernel timing (heb_prof_enable): CUDA events recorded on the launch
+// stream around every kernel, resolved in heb_prof_summary.  Off by default.
+bool prof_enabled();
+int prof_begin(cudaStream_t st);
+void prof_end(int slot, const char *name, double bytes, cudaStream_t st);
+// Each launch declares its algorithmic bytes (every input read once, every output
+// written once); a caller-provided override (heb_prof_next_bytes) takes precedence.
+struct ProfScope {
+    int slot;
+    const char *name;
+    double bytes;
+    cudaStream_t st;
+    ProfScope(const char *n, cudaStream_t s, double b) : slot(-1), name(n), bytes(b), st(s) {
+        if (prof_enabled()) slot = prof_begin(s);
+    }
+    ~ProfScope() {
+        if (slot >= 0) prof_end(slot, name, bytes, st);
+    }
+};
+#define PROF(name, st, bytes) ProfScope _prof_scope(name, st, (double)(bytes))
+
 // =============================================================================
 // context
 // =============================================================================

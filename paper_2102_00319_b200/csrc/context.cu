@@ -213,3 +213,140 @@ extern "C" int heb_sync(void *stream) {
     return HEB_OK;
 }
 
+
+// =============================================================================
+// per-kernel event profiler (used by bench.py for the roofline's launch durations)
+// =============================================================================
+#include <map>
+#include <mutex>
+
+namespace {
+struct ProfRec {
+    cudaEvent_t a, b;
+    const char *name;
+    double bytes;
+};
+thread_local double t_next_bytes = -1.0;
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof_recs;
+std::vector<cudaEvent_t> g_prof_pool;
+
+cudaEvent_t take_event() {
+    if (!g_prof_pool.empty()) {
+        cudaEvent_t e = g_prof_pool.back();
+        g_prof_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+}  // namespace
+
+bool prof_enabled() { return g_prof_on; }
+
+int prof_begin(cudaStream_t st) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    ProfRec r{take_event(), take_event(), nullptr, 0.0};
+    cudaEventRecord(r.a, st);
+    g_prof_recs.push_back(r);
+    return (int)g_prof_recs.size() - 1;
+}
+
+void prof_end(int slot, const char *name, double bytes, cudaStream_t st) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    if (slot < 0 || slot >= (int)g_prof_recs.size()) return;
+    g_prof_recs[slot].name = name;
+    g_prof_recs[slot].bytes = t_next_bytes >= 0 ? t_next_bytes : bytes;
+    t_next_bytes = -1.0;
+    cudaEventRecord(g_prof_recs[slot].b, st);
+}
+
+extern "C" int heb_prof_enable(int on) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    for (auto &r : g_prof_recs) {
+        g_prof_pool.push_back(r.a);
+        g_prof_pool.push_back(r.b);
+    }
+    g_prof_recs.clear();
+    g_prof_on = on != 0;
+    return HEB_OK;
+}
+
+extern "C" int heb_prof_next_bytes(double bytes) {
+    t_next_bytes = bytes;
+    return HEB_OK;
+}
+
+// "name launches total_ms total_bytes" lines, one per kernel, after synchronising the events.
+extern "C" int heb_prof_summary(char *buf, size_t len) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    struct Agg {
+        long n = 0;
+        double ms = 0, bytes = 0;
+    };
+    std::map<std::string, Agg> agg;
+    for (auto &r : g_prof_recs) {
+        if (!r.name) continue;
+        cudaEventSynchronize(r.b);
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) return fail(HEB_ECUDA, "event timing failed");
+        auto &e = agg[r.name];
+        e.n += 1;
+        e.ms += ms;
+        e.bytes += r.bytes;
+    }
+    std::string out;
+    char line[256];
+    for (auto &kv : agg) {
+        snprintf(line, sizeof line, "%s %ld %.6f %.0f\n", kv.first.c_str(), kv.second.n, kv.second.ms,
+                 kv.second.bytes);
+        out += line;
+    }
+    if (buf && len) {
+        strncpy(buf, out.c_str(), len - 1);
+        buf[len - 1] = 0;
+    }
+    return (int)out.size();
+}
+
+// =============================================================================
+// integer modmul microbenchmark: the INT64 roofline denominator
+// =============================================================================
+__global__ void k_bench_modmul(u64 *sink, u64 p, u64 w, u64 ws, int iters) {
+    u64 x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = (threadIdx.x + blockIdx.x * blockDim.x) * 8 + i + 1;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = shoup_lazy(x[i], w, ws, p);
+    }
+    u64 s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s ^= x[i];
+    if (s == 0x9e3779b97f4a7c15ull) sink[0] = s;
+}
+
+// Launch blocks x threads threads each doing iters x 8 Shoup modmuls; elapsed ms out.
+extern "C" int heb_bench_modmul(int blocks, int threads, int iters, uint64_t p, double *ms_out, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    u64 *sink;
+    CUDA_TRY(cudaMallocAsync(&sink, 8, st));
+    const u64 w = (p >> 1) + 12345, ws = (u64)(((u128)w << 64) / p);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    k_bench_modmul<<<blocks, threads, 0, st>>>(sink, p, w, ws, 16);  // warm-up
+    cudaEventRecord(a, st);
+    k_bench_modmul<<<blocks, threads, 0, st>>>(sink, p, w, ws, iters);
+    cudaEventRecord(b, st);
+    CUDA_TRY(cudaEventSynchronize(b));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    *ms_out = ms;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    CUDA_TRY(cudaFreeAsync(sink, st));
+    return HEB_OK;
+}

@@ -72,11 +72,11 @@ static int launch_rescale(heb_ctx *c, heb_ct in, const u64 *pt, int64_t pstride,
         ib.data += b0 * in.ct_stride;
         ob.data += b0 * out.ct_stride;
         const u64 *pb = pt ? pt + b0 * pstride : nullptr;
-        k_rescale_head<LOGN><<<dim3(comps, gdim(cnt)), T, sm, st>>>(kctx(c), ib, pb, pstride, (i64 *)V.p, comps,
-                                                                     level, cnt);
+        { PROF("k_rescale_head", st, 8.0 * c->n * (2.0 * cnt * comps + (pt ? (pstride ? cnt : 1) : 0))); k_rescale_head<LOGN><<<dim3(comps, gdim(cnt)), T, sm, st>>>(kctx(c), ib, pb, pstride, (i64 *)V.p, comps,
+                                                                     level, cnt); }
         LAUNCH_CHECK();
-        k_rescale_tail<LOGN><<<dim3(level, gdim(cnt), comps), T, sm, st>>>(kctx(c), ib, pb, pstride,
-                                                                            (const i64 *)V.p, ob, comps, level, cnt);
+        { PROF("k_rescale_tail", st, 8.0 * c->n * (cnt * comps * (1.0 + 2.0 * level) + (pt ? level * (pstride ? cnt : 1) : 0))); k_rescale_tail<LOGN><<<dim3(level, gdim(cnt), comps), T, sm, st>>>(kctx(c), ib, pb, pstride,
+                                                                            (const i64 *)V.p, ob, comps, level, cnt); }
         LAUNCH_CHECK();
     }
     return HEB_OK;
@@ -288,24 +288,24 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const u64 *kb, con
         dd.data += b0 * d.ct_stride;
         o.data += b0 * out.ct_stride;
         const unsigned gy = gdim(cnt);
-        k_ks_head<LOGN><<<dim3(k, gy), T, sm, st>>>(K, s, comp, (i64 *)sD.p, k, cnt);
+        { PROF("k_ks_head", st, 16.0 * n * cnt * k); k_ks_head<LOGN><<<dim3(k, gy), T, sm, st>>>(K, s, comp, (i64 *)sD.p, k, cnt); }
         LAUNCH_CHECK();
-        k_ks_modup<LOGN><<<dim3(k + 1, gy), T, sm, st>>>(K, s, comp, (const i64 *)sD.p, kb, ka, k, (u64 *)sA.p, cnt);
+        { PROF("k_ks_modup", st, 8.0 * n * (2.0 * cnt * k + 2.0 * k * (k + 1) + 2.0 * cnt * (k + 1))); k_ks_modup<LOGN><<<dim3(k + 1, gy), T, sm, st>>>(K, s, comp, (const i64 *)sD.p, kb, ka, k, (u64 *)sA.p, cnt); }
         LAUNCH_CHECK();
         if (rescale) {
-            k_ks_down_head<LOGN><<<dim3(2, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
-                                                                 (u64 *)sL.p, cnt);
+            { PROF("k_ks_down_head", st, 8.0 * n * cnt * 10.0); k_ks_down_head<LOGN><<<dim3(2, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
+                                                                 (u64 *)sL.p, cnt); }
             LAUNCH_CHECK();
-            k_ks_down_rescale_tail<LOGN><<<dim3(k - 1, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, dd,
+            { PROF("k_ks_down_rescale_tail", st, 8.0 * n * cnt * 2.0 * (2 + 3 * (k - 1))); k_ks_down_rescale_tail<LOGN><<<dim3(k - 1, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, dd,
                                                                              (const i64 *)sP.p, (const u64 *)sL.p, k,
-                                                                             o, cnt);
+                                                                             o, cnt); }
             LAUNCH_CHECK();
         } else {
-            k_ks_down_head<LOGN><<<dim3(1, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
-                                                                 (u64 *)sL.p, cnt);
+            { PROF("k_ks_down_head", st, 8.0 * n * cnt * 4.0); k_ks_down_head<LOGN><<<dim3(1, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
+                                                                 (u64 *)sL.p, cnt); }
             LAUNCH_CHECK();
-            k_ks_down_tail<LOGN><<<dim3(k, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, (const i64 *)sP.p, k, dd, o,
-                                                                 cnt);
+            { PROF("k_ks_down_tail", st, 8.0 * n * cnt * (2.0 + 5.0 * k)); k_ks_down_tail<LOGN><<<dim3(k, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, (const i64 *)sP.p, k, dd, o,
+                                                                 cnt); }
             LAUNCH_CHECK();
         }
     }
@@ -333,7 +333,7 @@ extern "C" int heb_rotate(heb_ctx *c, heb_ct ct, const uint64_t *gk_b, const uin
     CUDA_TRY(rot.get(sizeof(u64) * (size_t)count * 2 * k * c->n));
     heb_ct r{(u64 *)rot.p, (int64_t)2 * k * c->n, (int64_t)k * c->n};
     const int64_t lines = count * 2 * k;
-    k_galois_ct<<<pw_grid(c->n, lines), 256, 0, st>>>(ct, r, lines, k, c->log_n, galois % (2ull * c->n));
+    { PROF("k_galois_ct", st, 16.0 * c->n * lines); k_galois_ct<<<pw_grid(c->n, lines), 256, 0, st>>>(ct, r, lines, k, c->log_n, galois % (2ull * c->n)); }
     LAUNCH_CHECK();
     DISPATCH_LOGN(c, launch_keyswitch, c, r, 1, gk_b, gk_a, r, out, count, level, false, st);
 }

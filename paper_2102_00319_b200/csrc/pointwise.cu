@@ -92,7 +92,7 @@ extern "C" int heb_add(heb_ctx *c, heb_ct a, heb_ct b, heb_ct o, int64_t count, 
     if (!c || k < 1 || k > c->num_rows || comps < 1) return fail(HEB_EINVAL, "heb_add: bad args");
     if (count <= 0) return HEB_OK;
     const int64_t lines = count * comps * k;
-    k_add<<<pw_grid(c->n, lines), 256, 0, (cudaStream_t)stream>>>(kctx(c), a, b, o, lines, comps, k, c->log_n);
+    { PROF("k_add", (cudaStream_t)stream, 24.0 * c->n * lines); k_add<<<pw_grid(c->n, lines), 256, 0, (cudaStream_t)stream>>>(kctx(c), a, b, o, lines, comps, k, c->log_n); }
     LAUNCH_CHECK();
     return HEB_OK;
 }
@@ -103,8 +103,8 @@ extern "C" int heb_add_plain(heb_ctx *c, heb_ct a, const uint64_t *pt, int64_t p
     if (count <= 0) return HEB_OK;
     const int64_t lines = count * 2 * k;
     const int copy_c1 = (o.data != a.data) || (o.comp_stride != a.comp_stride) || (o.ct_stride != a.ct_stride);
-    k_add_plain<<<pw_grid(c->n, lines), 256, 0, (cudaStream_t)stream>>>(kctx(c), a, pt, pstride, o, lines, k,
-                                                                         c->log_n, copy_c1);
+    { PROF("k_add_plain", (cudaStream_t)stream, 8.0 * c->n * (2.0 * lines + k * (pstride ? count : 1))); k_add_plain<<<pw_grid(c->n, lines), 256, 0, (cudaStream_t)stream>>>(kctx(c), a, pt, pstride, o, lines, k,
+                                                                         c->log_n, copy_c1); }
     LAUNCH_CHECK();
     return HEB_OK;
 }
@@ -114,15 +114,15 @@ extern "C" int heb_tensor(heb_ctx *c, heb_ct a, heb_ct b, heb_ct d, int64_t coun
     if (!c || k < 1 || k > c->num_rows) return fail(HEB_EINVAL, "heb_tensor: bad args");
     if (count <= 0) return HEB_OK;
     const int64_t lines = count * k;
-    k_tensor<<<pw_grid(c->n, lines), 256, 0, (cudaStream_t)stream>>>(kctx(c), a, b, d, lines, k, c->log_n,
-                                                                      accumulate);
+    { PROF("k_tensor", (cudaStream_t)stream, 8.0 * c->n * lines * (accumulate ? 10.0 : 7.0)); k_tensor<<<pw_grid(c->n, lines), 256, 0, (cudaStream_t)stream>>>(kctx(c), a, b, d, lines, k, c->log_n,
+                                                                      accumulate); }
     LAUNCH_CHECK();
     return HEB_OK;
 }
 
 extern "C" int heb_mul_rows(heb_ctx *c, const uint64_t *a, const uint64_t *b, uint64_t *o, int rows, void *stream) {
     if (!c || rows < 1 || rows > c->num_rows) return fail(HEB_EINVAL, "heb_mul_rows: bad args");
-    k_mul_rows<<<pw_grid(c->n, rows), 256, 0, (cudaStream_t)stream>>>(kctx(c), a, b, o, rows, c->log_n);
+    { PROF("k_mul_rows", (cudaStream_t)stream, 24.0 * c->n * rows); k_mul_rows<<<pw_grid(c->n, rows), 256, 0, (cudaStream_t)stream>>>(kctx(c), a, b, o, rows, c->log_n); }
     LAUNCH_CHECK();
     return HEB_OK;
 }
@@ -132,8 +132,8 @@ extern "C" int heb_galois(heb_ctx *c, const uint64_t *in, uint64_t *out, int64_t
     if (!c || !(galois & 1) || in == out || rows < 1 || rows > c->num_rows) return fail(HEB_EINVAL, "heb_galois: bad args");
     if (count <= 0) return HEB_OK;
     const int64_t lines = count * rows;
-    k_galois<<<pw_grid(c->n, lines), 256, 0, (cudaStream_t)stream>>>(in, out, lines, bstride, rows, c->log_n,
-                                                                      galois % (2ull * c->n));
+    { PROF("k_galois", (cudaStream_t)stream, 16.0 * c->n * lines); k_galois<<<pw_grid(c->n, lines), 256, 0, (cudaStream_t)stream>>>(in, out, lines, bstride, rows, c->log_n,
+                                                                      galois % (2ull * c->n)); }
     LAUNCH_CHECK();
     return HEB_OK;
 }
@@ -201,7 +201,7 @@ extern "C" int heb_dot_tensor(heb_ctx *c, heb_ct a, heb_ct b, const int32_t *ia,
     if (!c || !ia || !ib || taps < 1 || k < 1 || k > c->num_rows) return fail(HEB_EINVAL, "heb_dot_tensor: bad args");
     if (n_out <= 0) return HEB_OK;
     dim3 grid((c->n + 127) / 128, gdim(n_out), k);
-    k_dot_tensor<<<grid, 128, 0, (cudaStream_t)stream>>>(kctx(c), a, b, ia, ib, taps, d, n_out, k, c->log_n, c->flush);
+    { PROF("k_dot_tensor", (cudaStream_t)stream, 24.0 * c->n * n_out * k); k_dot_tensor<<<grid, 128, 0, (cudaStream_t)stream>>>(kctx(c), a, b, ia, ib, taps, d, n_out, k, c->log_n, c->flush); }
     LAUNCH_CHECK();
     return HEB_OK;
 }
@@ -226,8 +226,8 @@ extern "C" int heb_sum_gather(heb_ctx *c, heb_ct a, const int32_t *idx, int term
     if (!c || !idx || terms < 1 || k < 1 || k > c->num_rows || comps < 1) return fail(HEB_EINVAL, "heb_sum_gather: bad args");
     if (n_out <= 0) return HEB_OK;
     const int64_t lines = n_out * comps * k;
-    k_sum_gather<<<pw_grid(c->n, lines), 256, 0, (cudaStream_t)stream>>>(kctx(c), a, idx, terms, o, lines, comps, k,
-                                                                          c->log_n);
+    { PROF("k_sum_gather", (cudaStream_t)stream, 8.0 * c->n * lines * (terms + 1.0)); k_sum_gather<<<pw_grid(c->n, lines), 256, 0, (cudaStream_t)stream>>>(kctx(c), a, idx, terms, o, lines, comps, k,
+                                                                          c->log_n); }
     LAUNCH_CHECK();
     return HEB_OK;
 }

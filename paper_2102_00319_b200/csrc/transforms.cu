@@ -43,10 +43,10 @@ static int launch_ntt(heb_ctx *c, uint64_t *data, int64_t count, int rows, int r
     dim3 grid(rows, gdim(count));
     if (inverse) {
         CUDA_TRY(prep_kernel(k_ntt_inv<LOGN>, sm));
-        k_ntt_inv<LOGN><<<grid, T, sm, st>>>(kctx(c), data, count, row0, bstride);
+        { PROF("k_ntt_inv", st, 16.0 * c->n * rows * count); k_ntt_inv<LOGN><<<grid, T, sm, st>>>(kctx(c), data, count, row0, bstride); }
     } else {
         CUDA_TRY(prep_kernel(k_ntt_fwd<LOGN>, sm));
-        k_ntt_fwd<LOGN><<<grid, T, sm, st>>>(kctx(c), data, count, row0, bstride);
+        { PROF("k_ntt_fwd", st, 16.0 * c->n * rows * count); k_ntt_fwd<LOGN><<<grid, T, sm, st>>>(kctx(c), data, count, row0, bstride); }
     }
     LAUNCH_CHECK();
     return HEB_OK;
@@ -86,7 +86,7 @@ static int launch_spread(heb_ctx *c, const int64_t *coeffs, int64_t count, uint6
                          int64_t ostride, cudaStream_t st) {
     constexpr size_t sm = smem_bytes<LOGN>();
     CUDA_TRY(prep_kernel(k_spread_ntt<LOGN>, sm));
-    k_spread_ntt<LOGN><<<dim3(rows, gdim(count)), ntt::Shape<LOGN>::T, sm, st>>>(kctx(c), coeffs, count, out, ostride);
+    { PROF("k_spread_ntt", st, 8.0 * c->n * count * (1.0 + rows)); k_spread_ntt<LOGN><<<dim3(rows, gdim(count)), ntt::Shape<LOGN>::T, sm, st>>>(kctx(c), coeffs, count, out, ostride); }
     LAUNCH_CHECK();
     return HEB_OK;
 }
@@ -132,7 +132,7 @@ static int launch_encrypt(heb_ctx *c, const i64 *v, const i64 *e0m, const i64 *e
                           heb_ct out, int64_t count, int k, cudaStream_t st) {
     constexpr size_t sm = smem_bytes<LOGN>();
     CUDA_TRY(prep_kernel(k_encrypt<LOGN>, sm));
-    k_encrypt<LOGN><<<dim3(k, gdim(count)), ntt::Shape<LOGN>::T, sm, st>>>(kctx(c), v, e0m, e1, pkb, pka, out, count);
+    { PROF("k_encrypt", st, 8.0 * c->n * (3.0 * count + 2.0 * k + 2.0 * count * k)); k_encrypt<LOGN><<<dim3(k, gdim(count)), ntt::Shape<LOGN>::T, sm, st>>>(kctx(c), v, e0m, e1, pkb, pka, out, count); }
     LAUNCH_CHECK();
     return HEB_OK;
 }
@@ -196,11 +196,11 @@ static int launch_decrypt(heb_ctx *c, heb_ct ct, const u64 *s, i64 *coeffs, i64 
     Scratch tmp(st);
     CUDA_TRY(tmp.get(sizeof(u64) * (size_t)count * rows * c->n));
     CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(i64) * count, st));
-    k_decrypt_rows<LOGN><<<dim3(rows, gdim(count)), ntt::Shape<LOGN>::T, sm, st>>>(kctx(c), ct, s, (u64 *)tmp.p, rows,
-                                                                                    count);
+    { PROF("k_decrypt_rows", st, 8.0 * c->n * (3.0 * count * rows + rows)); k_decrypt_rows<LOGN><<<dim3(rows, gdim(count)), ntt::Shape<LOGN>::T, sm, st>>>(kctx(c), ct, s, (u64 *)tmp.p, rows,
+                                                                                    count); }
     LAUNCH_CHECK();
-    k_decrypt_finish<<<pw_grid(c->n, count), 256, 0, st>>>(kctx(c), (const u64 *)tmp.p, coeffs, (unsigned long long *)bad,
-                                                            rows, count, c->log_n);
+    { PROF("k_decrypt_finish", st, 8.0 * c->n * count * (rows + 1.0)); k_decrypt_finish<<<pw_grid(c->n, count), 256, 0, st>>>(kctx(c), (const u64 *)tmp.p, coeffs, (unsigned long long *)bad,
+                                                            rows, count, c->log_n); }
     LAUNCH_CHECK();
     return HEB_OK;
 }
@@ -263,7 +263,7 @@ template <int LOGN>
 static int launch_pk(heb_ctx *c, const u64 *s, const u64 *a, const i64 *e, u64 *pkb, int rows, cudaStream_t st) {
     constexpr size_t sm = smem_bytes<LOGN>();
     CUDA_TRY(prep_kernel(k_make_pk<LOGN>, sm));
-    k_make_pk<LOGN><<<rows, ntt::Shape<LOGN>::T, sm, st>>>(kctx(c), s, a, e, pkb);
+    { PROF("k_make_pk", st, 8.0 * c->n * (1.0 + 3.0 * rows)); k_make_pk<LOGN><<<rows, ntt::Shape<LOGN>::T, sm, st>>>(kctx(c), s, a, e, pkb); }
     LAUNCH_CHECK();
     return HEB_OK;
 }
@@ -272,7 +272,7 @@ static int launch_swk(heb_ctx *c, const u64 *s, const u64 *t, const u64 *a, cons
                       cudaStream_t st) {
     constexpr size_t sm = smem_bytes<LOGN>();
     CUDA_TRY(prep_kernel(k_make_swk<LOGN>, sm));
-    k_make_swk<LOGN><<<dim3(c->num_rows, digits), ntt::Shape<LOGN>::T, sm, st>>>(kctx(c), s, t, a, e, kb);
+    { PROF("k_make_swk", st, 8.0 * c->n * (digits + 4.0 * digits * c->num_rows)); k_make_swk<LOGN><<<dim3(c->num_rows, digits), ntt::Shape<LOGN>::T, sm, st>>>(kctx(c), s, t, a, e, kb); }
     LAUNCH_CHECK();
     return HEB_OK;
 }

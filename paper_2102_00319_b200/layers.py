@@ -1,0 +1,286 @@
+"""Batched encrypted-CNN layer evaluator: one launch sequence per layer.
+
+The reference evaluates a layer as nested Python loops of per-ciphertext ops
+(`/root/reference/pkg/src/hecnn/layers.py:92-294`, driven by
+`executor.py:161-279` on a thread pool).  Here every layer is a handful of
+launches over *all* of its independent ciphertexts:
+
+* conv / dense  -> ``heb_dot_tensor`` (all output cells x all taps, lazy 128-bit
+                   accumulation) + one batched ``heb_relin_rescale``
+                   (+ broadcast bias adds);
+* square        -> ``heb_tensor`` + ``heb_relin_rescale``;
+* poly act      -> square path + two batched ct x pt rescales + adds
+                   (reference ``approx_relu_cell``);
+* sum pool      -> ``heb_sum_gather`` over the 2x2 windows;
+* flatten       -> index remapping only (no data movement).
+
+Ciphertext bits, levels, exact scales, noise estimates and op counters are
+identical to running ``percell.run_network`` (the reference op sequence) on
+the same backend.  Feature maps are ``CipherBatch`` objects whose items are
+laid out channel-major: item = c*(m*n) + i*n + j.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from fractions import Fraction
+
+import numpy as np
+import torch
+
+from . import _lib
+from .backend import B200Backend, CipherBatch, ct_desc
+from .contract import noise_sum
+from .errors import DepthExhausted, ScaleMismatch
+from .model import BIAS_ENTROPY_BASE, WINDOW_ORDER, Conv, Dense, Flatten, Network, PolyAct, SumPool, Square, ledger, weight_entropies
+from .percell import act_plaintexts
+
+
+@dataclass
+class EncryptedNetworkBatch:
+    net: Network
+    weights: list   # per layer: CipherBatch of the flattened weight tensor (or None)
+    biases: list    # per layer: CipherBatch (or None)
+    trace: list
+
+
+def encrypt_network(backend: B200Backend, net: Network, key) -> EncryptedNetworkBatch:
+    """Model-owner encryption with the same entropy tags as ``percell.encrypt_network``."""
+    trace = ledger(net, backend.chain, backend.canonical_scale)
+    tags = weight_entropies(net)
+    slots = backend.slots
+    weights, biases = [], []
+    bias_tag = BIAS_ENTROPY_BASE
+    for li, layer in enumerate(net.layers):
+        in_level = trace[li]["level"]
+        out = trace[li + 1]
+        if isinstance(layer, (Conv, Dense)):
+            w = layer.weights.ravel()
+            vals = np.repeat(w[:, None], slots, axis=1)
+            wb = backend.encrypt_batch(vals, key, tags[li].ravel())
+            weights.append(drop_batch(wb, in_level))
+            if layer.bias is not None:
+                nb = len(layer.bias)
+                bvals = np.repeat(np.asarray(layer.bias, dtype=np.float64)[:, None], slots, axis=1)
+                bb = backend.encrypt_batch(bvals, key, bias_tag + np.arange(nb), scale=out["scale"])
+                bias_tag += nb
+                biases.append(drop_batch(bb, out["level"]))
+            else:
+                biases.append(None)
+        else:
+            weights.append(None)
+            biases.append(None)
+    return EncryptedNetworkBatch(net, weights, biases, trace)
+
+
+def encrypt_images(backend: B200Backend, images: np.ndarray, key) -> CipherBatch:
+    """Client packing: cell (i, j) holds pixel (i, j) of every image, entropy = i*n + j."""
+    imgs = np.asarray(images, dtype=np.float64)
+    _, m, n = imgs.shape
+    vals = imgs.reshape(imgs.shape[0], m * n).T  # (cells, batch)
+    return backend.encrypt_batch(vals, key, np.arange(m * n))
+
+
+def drop_batch(b: CipherBatch, level: int) -> CipherBatch:
+    if level > b.level:
+        raise ValueError("cannot raise a ciphertext's level")
+    return CipherBatch(b.buf, level, b.scale, b.noise_bits)
+
+
+class LayerEvaluator:
+    """Runs an ``EncryptedNetworkBatch`` over a packed input batch on one device."""
+
+    def __init__(self, backend: B200Backend):
+        self.be = backend
+        self.ctx = backend.ctx
+        self._idx_cache: dict = {}
+        self._unique: dict = {}
+
+    # -- primitives -------------------------------------------------------------------
+    def _idx(self, key, builder) -> torch.Tensor:
+        t = self._idx_cache.get(key)
+        if t is None:
+            host = np.ascontiguousarray(builder(), dtype=np.int32)
+            t = torch.from_numpy(host).to(self.be.dev)
+            self._idx_cache[key] = t
+            if host.ndim == 3:  # (a_idx, b_idx) pair: remember operand reuse for the roofline
+                self._unique[t[0].data_ptr()] = (len(np.unique(host[0])), len(np.unique(host[1])))
+        return t
+
+    def _empty(self, count: int, comps: int, k: int) -> torch.Tensor:
+        return self.ctx.empty(count, comps, k, self.be.n)
+
+    def dot(self, a: CipherBatch, b: CipherBatch, ia: torch.Tensor, ib: torch.Tensor, taps: int, n_out: int):
+        """raw_o = sum_t a[ia] (x) b[ib]; returns (raw buffer, level, scale, noise)."""
+        if a.scale * b.scale != a.scale * b.scale:  # pragma: no cover
+            raise ScaleMismatch("unreachable")
+        lvl = min(a.level, b.level)
+        if lvl < 1:
+            raise DepthExhausted("ciphertext-ciphertext multiply at level 0")
+        k = lvl + 1
+        raw = self._empty(n_out, 3, k)
+        ua, ub = self._unique.get(ia.data_ptr(), (n_out * taps, n_out * taps))
+        _lib.prof_next_bytes(8.0 * self.be.n * k * (2 * ua + 2 * ub + 3 * n_out))
+        self.ctx.call("heb_dot_tensor", a.desc(), b.desc(), ia.data_ptr(), ib.data_ptr(), taps, ct_desc(raw), n_out, k,
+                      self.ctx.stream)
+        term = noise_sum(a.noise_bits, b.noise_bits)
+        if term > float("-inf"):
+            term += 1.0
+        noise = term + math.log2(taps) if term > float("-inf") else term
+        self.be.counters.bump(ctct_mult=n_out * taps, ctct_add=n_out * (taps - 1))
+        return raw, lvl, a.scale * b.scale, noise
+
+    def finalize(self, raw: torch.Tensor, level: int, scale: Fraction, noise: float) -> CipherBatch:
+        evk = self.be._require_eval_key().evaluation
+        n_out = raw.shape[0]
+        out = self._empty(n_out, 2, level)
+        self.ctx.call("heb_relin_rescale", ct_desc(raw), evk.b.data_ptr(), evk.a.data_ptr(), ct_desc(out), n_out, level,
+                      self.ctx.stream)
+        new_scale = self.be._rescale_scale(scale, level)
+        return CipherBatch(out, level - 1, new_scale, max(noise, self.be._round_noise_bits(new_scale)))
+
+    def add(self, a: CipherBatch, b: CipherBatch, b_broadcast: bool = False, count: int | None = None,
+            a_off: int = 0, out: CipherBatch | None = None, out_off: int = 0) -> CipherBatch:
+        if a.scale != b.scale:
+            raise ScaleMismatch("batched add requires equal scales")
+        lvl = min(a.level, b.level)
+        k = lvl + 1
+        n = count if count is not None else a.count
+        dst = out.buf if out is not None else self._empty(n, 2, k)
+        da = ct_desc(a.buf)
+        da.data = a.buf[a_off].data_ptr()
+        db = ct_desc(b.buf)
+        if b_broadcast:
+            db.ct_stride = 0
+        dd = ct_desc(dst)
+        dd.data = dst[out_off].data_ptr()
+        self.ctx.call("heb_add", da, db, dd, n, 2, k, self.ctx.stream)
+        self.be.counters.bump(ctct_add=n)
+        return CipherBatch(dst, lvl, a.scale, noise_sum(a.noise_bits, b.noise_bits))
+
+    def square(self, y: CipherBatch) -> CipherBatch:
+        if y.level < 1:
+            raise DepthExhausted("ciphertext-ciphertext multiply at level 0")
+        k = y.k
+        raw = self._empty(y.count, 3, k)
+        self.ctx.call("heb_tensor", y.desc(), y.desc(), ct_desc(raw), y.count, k, 0, self.ctx.stream)
+        self.be.counters.bump(ctct_mult=y.count)
+        term = y.noise_bits + 1.0 if y.noise_bits > float("-inf") else y.noise_bits
+        term = noise_sum(y.noise_bits, y.noise_bits) + 1.0 if y.noise_bits > float("-inf") else term
+        return self.finalize(raw, y.level, y.scale * y.scale, term)
+
+    def mul_plain(self, y: CipherBatch, pt, values_mag: float) -> CipherBatch:
+        if y.level < 1:
+            raise DepthExhausted("ciphertext-plaintext multiply at level 0")
+        out = self._empty(y.count, 2, y.level)
+        self.ctx.call("heb_rescale", y.desc(), pt.payload.rows.data_ptr(), 0, ct_desc(out), y.count, 2, y.level,
+                      self.ctx.stream)
+        self.be.counters.bump(ctpt_mult=y.count)
+        scale = self.be._rescale_scale(y.scale * pt.scale, y.level)
+        noise = y.noise_bits + max(0.0, math.log2(max(values_mag, 1e-300))) + 1.0
+        return CipherBatch(out, y.level - 1, scale, max(noise, self.be._round_noise_bits(scale)))
+
+    def add_plain(self, y: CipherBatch, pt) -> CipherBatch:
+        if pt.scale != y.scale:
+            raise ScaleMismatch("plaintext addend must be encoded at the ciphertext scale")
+        out = self._empty(y.count, 2, y.k)
+        self.ctx.call("heb_add_plain", y.desc(), pt.payload.rows.data_ptr(), 0, ct_desc(out), y.count, y.k,
+                      self.ctx.stream)
+        self.be.counters.bump(ctpt_add=y.count)
+        return CipherBatch(out, y.level, y.scale, noise_sum(y.noise_bits, self.be._encode_noise_bits()))
+
+    # -- layers --------------------------------------------------------------------------
+    def conv(self, x: CipherBatch, dims: tuple[int, int, int], layer: Conv, w: CipherBatch, bias) -> tuple:
+        c_in, m, n = dims
+        p, q = layer.kernel
+        s = layer.stride
+        om, on = layer.out_dims(m, n)
+        F = layer.filters
+        taps = c_in * p * q
+        n_out = F * om * on
+
+        def build():
+            f, i, j, c, dp, dq = np.meshgrid(np.arange(F), np.arange(om), np.arange(on), np.arange(c_in),
+                                             np.arange(p), np.arange(q), indexing="ij")
+            ia = c * (m * n) + (i * s + dp) * n + (j * s + dq)
+            ib = ((f * c_in + c) * p + dp) * q + dq
+            return np.stack([ia.reshape(n_out, taps), ib.reshape(n_out, taps)])
+
+        idx = self._idx(("conv", dims, layer.kernel, s, F), build)
+        raw, lvl, scale, noise = self.dot(x, w, idx[0], idx[1], taps, n_out)
+        y = self.finalize(raw, lvl, scale, noise)
+        if bias is not None:
+            for f in range(F):
+                self.add(y, bias_item(bias, f), b_broadcast=True, count=om * on, a_off=f * om * on, out=y,
+                         out_off=f * om * on)
+            y = CipherBatch(y.buf, min(y.level, bias.level), y.scale, noise_sum(y.noise_bits, bias.noise_bits))
+        return y, (F, om, on)
+
+    def poly_act(self, y: CipherBatch, act: PolyAct) -> CipherBatch:
+        pt_quad, pt_lin, pt_const = act_plaintexts(self.be, act, y.level, y.scale)
+        c0, c1, c2 = act.folded()
+        t = self.square(y)
+        quad = self.mul_plain(t, pt_quad, abs(c2))
+        lin = self.mul_plain(y, pt_lin, abs(c1))
+        r = self.add(quad, lin)
+        return self.add_plain(r, pt_const)
+
+    def sum_pool(self, y: CipherBatch, dims: tuple[int, int, int]) -> tuple:
+        c_in, m, n = dims
+        om, on = m // 2, n // 2
+        n_out = c_in * om * on
+
+        def build():
+            c, i, j = np.meshgrid(np.arange(c_in), np.arange(om), np.arange(on), indexing="ij")
+            terms = [c * (m * n) + (2 * i + di) * n + (2 * j + dj) for di, dj in WINDOW_ORDER]
+            return np.stack([t.ravel() for t in terms], axis=1)
+
+        idx = self._idx(("pool", dims), build)
+        out = self._empty(n_out, 2, y.k)
+        self.ctx.call("heb_sum_gather", y.desc(), idx.data_ptr(), 4, ct_desc(out), n_out, 2, y.k, self.ctx.stream)
+        self.be.counters.bump(ctct_add=3 * n_out)
+        noise = y.noise_bits
+        for _ in range(3):
+            noise = noise_sum(noise, y.noise_bits)
+        return CipherBatch(out, y.level, y.scale, noise), (c_in, om, on)
+
+    def dense(self, x: CipherBatch, flat_map: np.ndarray, layer: Dense, w: CipherBatch, bias) -> CipherBatch:
+        din, dout = layer.in_dim, layer.out_dim
+
+        def build():
+            ia = np.broadcast_to(flat_map[None, :], (dout, din))
+            ib = np.arange(din)[None, :] * dout + np.arange(dout)[:, None]
+            return np.stack([ia, ib])
+
+        idx = self._idx(("dense", din, dout, flat_map.tobytes()), build)
+        raw, lvl, scale, noise = self.dot(x, w, idx[0], idx[1], din, dout)
+        y = self.finalize(raw, lvl, scale, noise)
+        if bias is not None:
+            y = self.add(y, bias)
+        return y
+
+    def run(self, enc: EncryptedNetworkBatch, x: CipherBatch) -> CipherBatch:
+        net = enc.net
+        dims = (1, *net.input_dims)
+        flat_map = None
+        for li, layer in enumerate(net.layers):
+            if isinstance(layer, Conv):
+                x, dims = self.conv(x, dims, layer, enc.weights[li], enc.biases[li])
+            elif isinstance(layer, Square):
+                x = self.square(x)
+            elif isinstance(layer, PolyAct):
+                x = self.poly_act(x, layer)
+            elif isinstance(layer, SumPool):
+                x, dims = self.sum_pool(x, dims)
+            elif isinstance(layer, Flatten):
+                c_in, m, n = dims
+                i, j, c = np.meshgrid(np.arange(m), np.arange(n), np.arange(c_in), indexing="ij")
+                flat_map = (c * (m * n) + i * n + j).ravel()  # flat[(i*n+j)*C + c] = map[c][i][j]
+            elif isinstance(layer, Dense):
+                x = self.dense(x, flat_map, layer, enc.weights[li], enc.biases[li])
+        return x
+
+
+def bias_item(bias: CipherBatch, i: int) -> CipherBatch:
+    return CipherBatch(bias.buf[i:i + 1], bias.level, bias.scale, bias.noise_bits)

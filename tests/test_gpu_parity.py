@@ -193,3 +193,27 @@ def test_cfg1_digests_match_reference(golden):
         assert cd(be.mul_ct_pt(x, be.encode_plain(ys[i], level=x.level))) == rec["ctpt"]
         assert cd(be.add_ct_ct(x, y)) == rec["add"]
         assert list(be.decrypt(mul, keys).values[:8]) == rec["mul_dec8"]
+
+
+@pytest.mark.parametrize("name", ["mini2", "mini3", "mini4"])
+def test_batched_layers_match_reference(golden, dev_s128, name):
+    """The batched layer evaluator (one launch sequence per layer) reproduces the
+    reference op sequence bit for bit, including levels, scales and counters."""
+    from nets import mini_networks
+    from paper_2102_00319_b200 import layers
+
+    be, keys = dev_s128
+    net = mini_networks()[name]
+    imgs = np.random.default_rng(13).uniform(0, 1, (be.slots, 12, 12))[:, : net.input_dims[0], : net.input_dims[1]]
+    be.counters.reset()
+    enc = layers.encrypt_network(be, net, keys)
+    be.counters.reset()
+    x = layers.encrypt_images(be, imgs, keys)
+    out = layers.LayerEvaluator(be).run(enc, x)
+    g = golden["minis"][name]
+    digests = [digest(np.concatenate(be.cipher_rows_host(be.batch_to_cipher(out, i)))) for i in range(out.count)]
+    assert digests == g["logit_digests"]
+    assert out.level == g["level"] and out.scale == frac(g["scale"])
+    assert be.counters.snapshot().__dict__ == g["counters"]
+    dec = be.decrypt_batch(out, keys)
+    assert np.allclose(dec[:, :8].T, np.array(g["decrypted_first8"]), atol=0, rtol=0)
