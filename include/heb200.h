@@ -55,8 +55,8 @@ int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows, const uin
                    const uint64_t *psi);
 int heb_ctx_destroy(heb_ctx *ctx);
 int heb_ctx_ring_degree(const heb_ctx *ctx);
-/* Key-switch batches are processed in chunks of this many items so the
- * intermediates stay L2-resident (default 64). */
+/* Key-switch / rescale batches are processed in chunks of this many items
+ * (default 1024), bounding the stream-ordered scratch. */
 int heb_ctx_set_chunk(heb_ctx *ctx, int items);
 
 /* --- memory ----------------------------------------------------------------- */
@@ -93,16 +93,22 @@ int heb_tensor(heb_ctx *ctx, heb_ct a, heb_ct b, heb_ct raw, int64_t count, int 
  * plaintext rows (mul_ct_pt = mul_rows + rescale, ckks.py:320-331). */
 int heb_rescale(heb_ctx *ctx, heb_ct in, const uint64_t *pt, int64_t pt_stride, heb_ct out, int64_t count,
                 int comps, int level, void *stream);
+/* Prepare a switching key for the device key switch: from the reference layout
+ * (EvalKeyPayload b/a arrays, (digits, num_rows, N) Montgomery residues, ckks.py:72-75)
+ * to (digits, num_rows, 2, N) pairs (w, floor(w*2^64/p)) with w = residue * R^-1, so
+ * each key product is a single Shoup multiplication.  out holds digits*num_rows*4*N words. */
+int heb_prepare_switch_key(heb_ctx *ctx, const uint64_t *kb, const uint64_t *ka, int digits, uint64_t *out,
+                           void *stream);
 /* raw_finalize (ckks.py:359-387): key switch of d2 with the relinearisation key
- * (relin_accumulate + moddown_special), add d0/d1, rescale.  evk_b/evk_a are the
- * reference EvalKeyPayload arrays (digits, num_rows, N). Output level = level-1. */
-int heb_relin_rescale(heb_ctx *ctx, heb_ct raw, const uint64_t *evk_b, const uint64_t *evk_a, heb_ct out,
-                      int64_t count, int level, void *stream);
+ * (relin_accumulate + moddown_special), add d0/d1, rescale.  evk = prepared key
+ * (heb_prepare_switch_key).  Output level = level-1. */
+int heb_relin_rescale(heb_ctx *ctx, heb_ct raw, const uint64_t *evk, heb_ct out, int64_t count, int level,
+                      void *stream);
 /* Galois automorphism X -> X^galois on both components followed by a key switch
- * with the matching switching key (same layout as evk); level kept.  No reference
+ * with the matching prepared switching key; level kept.  No reference
  * counterpart (rotation is a non-goal there). */
-int heb_rotate(heb_ctx *ctx, heb_ct ct, const uint64_t *gk_b, const uint64_t *gk_a, heb_ct out, int64_t count,
-               int level, uint64_t galois, void *stream);
+int heb_rotate(heb_ctx *ctx, heb_ct ct, const uint64_t *gk, heb_ct out, int64_t count, int level,
+               uint64_t galois, void *stream);
 /* Evaluation-domain permutation only (rows 0..rows-1 of `count` blocks). */
 int heb_galois(heb_ctx *ctx, const uint64_t *in, uint64_t *out, int64_t count, int rows, int64_t block_stride,
                uint64_t galois, void *stream);

@@ -48,8 +48,9 @@ SIGNATURES: dict[str, list] = {
     "heb_add_plain": [_P, _CT, _P, _L, _CT, _L, _I, _P],
     "heb_tensor": [_P, _CT, _CT, _CT, _L, _I, _I, _P],
     "heb_rescale": [_P, _CT, _P, _L, _CT, _L, _I, _I, _P],
-    "heb_relin_rescale": [_P, _CT, _P, _P, _CT, _L, _I, _P],
-    "heb_rotate": [_P, _CT, _P, _P, _CT, _L, _I, _U, _P],
+    "heb_prepare_switch_key": [_P, _P, _P, _I, _P, _P],
+    "heb_relin_rescale": [_P, _CT, _P, _CT, _L, _I, _P],
+    "heb_rotate": [_P, _CT, _P, _CT, _L, _I, _U, _P],
     "heb_galois": [_P, _P, _P, _L, _I, _L, _U, _P],
     "heb_mul_rows": [_P, _P, _P, _P, _I, _P],
     "heb_encrypt": [_P, _P, _P, _P, _P, _P, _CT, _L, _I, _P],

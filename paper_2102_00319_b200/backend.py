@@ -150,8 +150,9 @@ class DevPublic:
 
 @dataclass(frozen=True)
 class DevSwitchKey:
-    b: "torch.Tensor"  # (digits, all rows, N)
+    b: "torch.Tensor"     # (digits, all rows, N) reference layout (Montgomery residues)
     a: "torch.Tensor"
+    prep: "torch.Tensor"  # (digits, all rows, 2, N, 2) Shoup pairs for the device key switch
 
 
 @dataclass
@@ -226,7 +227,14 @@ class B200Backend(HEBackend):
         kb = self.ctx.empty(digits, ch.num_rows, self.n)
         self.ctx.call("heb_make_switch_key", s_eval.data_ptr(), target.data_ptr(), a_d.data_ptr(), e_d.data_ptr(),
                       kb.data_ptr(), digits, self.ctx.stream)
-        return DevSwitchKey(b=kb, a=a_d)
+        return self.prepare_switch_key(kb, a_d)
+
+    def prepare_switch_key(self, kb: "torch.Tensor", ka: "torch.Tensor") -> DevSwitchKey:
+        """Attach the Shoup-pair form used by the device key switch (heb_prepare_switch_key)."""
+        digits = kb.shape[0]
+        prep = self.ctx.empty(digits, self.chain.num_rows, 2, self.n, 2)
+        self.ctx.call("heb_prepare_switch_key", kb.data_ptr(), ka.data_ptr(), digits, prep.data_ptr(), self.ctx.stream)
+        return DevSwitchKey(b=kb, a=ka, prep=prep)
 
     def galois_key(self, s_eval, galois: int) -> DevSwitchKey:
         target = self.ctx.empty(self.chain.num_rows, self.n)
@@ -378,16 +386,16 @@ class B200Backend(HEBackend):
         evk: DevSwitchKey = self._require_eval_key().evaluation
         k = x.level + 1
         out = self.ctx.empty(2, k - 1, self.n)
-        self.ctx.call("heb_relin_rescale", ct_desc(x.payload.buf), evk.b.data_ptr(), evk.a.data_ptr(), ct_desc(out),
-                      1, x.level, self.ctx.stream)
+        self.ctx.call("heb_relin_rescale", ct_desc(x.payload.buf), evk.prep.data_ptr(), ct_desc(out), 1, x.level,
+                      self.ctx.stream)
         return DevCipher(out, k - 1)
 
     def _rotate_impl(self, ct, galois) -> DevCipher:
         gk: DevSwitchKey = self._galois_keys[galois]
         k = ct.level + 1
         out = self.ctx.empty(2, k, self.n)
-        self.ctx.call("heb_rotate", ct_desc(ct.payload.buf), gk.b.data_ptr(), gk.a.data_ptr(), ct_desc(out), 1,
-                      ct.level, galois, self.ctx.stream)
+        self.ctx.call("heb_rotate", ct_desc(ct.payload.buf), gk.prep.data_ptr(), ct_desc(out), 1, ct.level, galois,
+                      self.ctx.stream)
         return DevCipher(out, k)
 
     # -- host views (tests / serialization) -------------------------------------------------

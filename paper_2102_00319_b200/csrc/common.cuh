@@ -66,7 +66,7 @@ struct LastConst {  // final inverse-stage factors (Shoup pairs)
 };
 
 struct heb_ctx {
-    int device = 0, log_n = 0, n = 0, num_rows = 0, chunk = 64;
+    int device = 0, log_n = 0, n = 0, num_rows = 0, chunk = 1024;
     std::vector<u64> primes;
     PrimeInfo *d_pi = nullptr;
     ulonglong2 *d_tw = nullptr, *d_itw = nullptr;
@@ -122,6 +122,9 @@ __device__ __forceinline__ void store16(u64 *__restrict__ dst, const u64 (&v)[16
 #pragma unroll
     for (int i = 0; i < 8; ++i) d[i] = make_ulonglong2(v[2 * i], v[2 * i + 1]);
 }
+
+// minimum resident CTAs per SM for the NTT kernels: caps registers at 64/thread
+#define NTT_MINB(LOGN) ((1024 >> ((LOGN) - 4)) > 32 ? 32 : (1024 >> ((LOGN) - 4)))
 
 template <int LOGN>
 static constexpr size_t smem_bytes() {

@@ -7,7 +7,7 @@
 //   tail: out_i = c_i [* pt_i] * qL^-1 - NTT_i(v * qL^-1 * R)  (k-1 NTTs / component)
 // =============================================================================
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_rescale_head(Ctx K, heb_ct in, const u64 *pt,
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_rescale_head(Ctx K, heb_ct in, const u64 *pt,
                                                                         int64_t pstride, i64 *V, int comps, int L,
                                                                         int64_t count) {
     extern __shared__ u64 sm[];
@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_rescale_head(Ctx K, heb
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_rescale_tail(Ctx K, heb_ct in, const u64 *pt,
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_rescale_tail(Ctx K, heb_ct in, const u64 *pt,
                                                                         int64_t pstride, const i64 *V, heb_ct out,
                                                                         int comps, int L, int64_t count) {
     extern __shared__ u64 sm[];
@@ -104,7 +104,7 @@ extern "C" int heb_rescale(heb_ctx *c, heb_ct in, const uint64_t *pt, int64_t ps
 // since every step is an identity mod q_i.
 // =============================================================================
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_ks_head(Ctx K, heb_ct src, int comp, i64 *D, int k,
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_head(Ctx K, heb_ct src, int comp, i64 *D, int k,
                                                                    int64_t count) {
     extern __shared__ u64 sm[];
     const int j = blockIdx.x;
@@ -119,50 +119,100 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_ks_head(Ctx K, heb_ct s
     }
 }
 
-// acc layout: (count, 2, k+1, N); row k is the special prime
+// acc layout: (count, 2, k+1, N); row k is the special prime.
+// key: prepared switching key (heb_prepare_switch_key): for digit j, chain row r the
+// ulonglong2 pairs (w, floor(w 2^64 / p)) of the b part (N entries) then the a part,
+// with w the key residue in standard form, so dig * key is one Shoup product that
+// keeps dig's Montgomery factor (identical to the reference's mont_mul(dig, evk)).
+// The accumulators stay in registers across the digit loop, so this kernel uses the
+// E = 8 engine variant (N/8 threads, 8 positions per thread) to keep the per-thread
+// working set small enough for full occupancy without spills.
+#define MODUP_E(LOGN) ((LOGN) >= 14 ? 16 : 8)
+#define MODUP_MINB(LOGN) ((1024 / ntt::Shape<LOGN, MODUP_E(LOGN)>::T) > 32 ? 32 : (1024 / ntt::Shape<LOGN, MODUP_E(LOGN)>::T))
+
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_ks_modup(Ctx K, heb_ct src, int comp, const i64 *D,
-                                                                    const u64 *kb, const u64 *ka, int k,
-                                                                    u64 *acc, int64_t count) {
+__global__ void __launch_bounds__(ntt::Shape<LOGN, MODUP_E(LOGN)>::T, MODUP_MINB(LOGN))
+    k_ks_modup(Ctx K, heb_ct src, int comp, const i64 *D, const ulonglong2 *key, int k, u64 *acc, int64_t count) {
+    constexpr int E = MODUP_E(LOGN);
     extern __shared__ u64 sm[];
     const int t = blockIdx.x;
     const int gt = t < k ? t : K.num_rows - 1;
     const PrimeInfo P = K.pi[gt];
+    const u64 p2 = 2 * P.p;
     const int n = 1 << LOGN;
-    const int pos = threadIdx.x * 16;
+    const int pos = threadIdx.x * E;
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
-        u64 a0[16], a1[16];
+        u64 a0[E], a1[E];
 #pragma unroll
-        for (int m = 0; m < 16; ++m) a0[m] = a1[m] = 0;
+        for (int m = 0; m < E; ++m) a0[m] = a1[m] = 0;
         for (int j = 0; j < k; ++j) {
-            u64 dig[16];
+            u64 dig[E];
             if (j == t) {
-                load16(at(src, b, comp, j, LOGN) + pos, dig);
+                const u64 *s = at(src, b, comp, j, LOGN) + pos;
+#pragma unroll
+                for (int m = 0; m < E; ++m) dig[m] = s[m];
             } else {
                 const i64 *dj = D + (b * k + j) * n;
-                ntt::forward<LOGN>(sm, tw_row<LOGN>(K, gt), P.p,
-                                   [&](int i) { return signed_mul_const(dj[i], P.rmod, P.rmod_s, P.p); }, dig);
+                ntt::forward<LOGN, E>(sm, tw_row<LOGN>(K, gt), P.p,
+                                      [&](int i) { return signed_mul_const(dj[i], P.rmod, P.rmod_s, P.p); }, dig);
             }
-            const size_t koff = ((size_t)j * K.num_rows + gt) * n + pos;
-            u64 eb[16], ea[16];
-            load16(kb + koff, eb);
-            load16(ka + koff, ea);
+            const ulonglong2 *kb = key + (((size_t)j * K.num_rows + gt) * 2) * n + pos;
+            const ulonglong2 *ka = kb + n;
 #pragma unroll
-            for (int m = 0; m < 16; ++m) {
-                a0[m] = add_mod(a0[m], mont_mul(dig[m], eb[m], P.p, P.pinv), P.p);
-                a1[m] = add_mod(a1[m], mont_mul(dig[m], ea[m], P.p, P.pinv), P.p);
+            for (int m = 0; m < E; ++m) {
+                const ulonglong2 wb = kb[m], wa = ka[m];
+                a0[m] = csub(a0[m] + shoup_lazy(dig[m], wb.x, wb.y, P.p), p2);
+                a1[m] = csub(a1[m] + shoup_lazy(dig[m], wa.x, wa.y, P.p), p2);
             }
         }
         u64 *o0 = acc + ((b * 2 + 0) * (k + 1) + t) * n + pos;
         u64 *o1 = acc + ((b * 2 + 1) * (k + 1) + t) * n + pos;
-        store16(o0, a0);
-        store16(o1, a1);
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            o0[m] = csub(a0[m], P.p);
+            o1[m] = csub(a1[m], P.p);
+        }
     }
+}
+
+// Prepared switching key: Montgomery residue x -> (w = x R^-1, floor(w 2^64 / p)).
+// floor(w 2^64/p) = w floor(2^64/p) + floor(w (2^64 mod p) / p), the last term by a
+// Shoup quotient with one correction -- exact, no 128-bit division.
+__global__ void k_prep_key(Ctx K, const u64 *kb, const u64 *ka, ulonglong2 *out, int digits, int logn) {
+    const int n = 1 << logn;
+    const int r = blockIdx.y, j = blockIdx.z;
+    const PrimeInfo P = K.pi[r];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const size_t src = ((size_t)j * K.num_rows + r) * n + i;
+        ulonglong2 *dst = out + (((size_t)j * K.num_rows + r) * 2) * n + i;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const u64 w = mont_mul(c == 0 ? kb[src] : ka[src], 1, P.p, P.pinv);
+            u64 q = __umul64hi(w, P.rmod_s);
+            const u64 rem = w * P.rmod - q * P.p;
+            q += rem >= P.p;
+            dst[(size_t)c * n] = make_ulonglong2(w, w * P.r1s + q);
+        }
+    }
+}
+
+extern "C" int heb_prepare_switch_key(heb_ctx *c, const uint64_t *kb, const uint64_t *ka, int digits, uint64_t *out,
+                                      void *stream) {
+    if (!c || !kb || !ka || !out || digits < 1 || digits > c->num_rows - 1)
+        return fail(HEB_EINVAL, "heb_prepare_switch_key: bad args");
+    cudaStream_t st = (cudaStream_t)stream;
+    {
+        PROF("k_prep_key", st, 8.0 * c->n * digits * c->num_rows * 6.0);
+        k_prep_key<<<dim3((c->n + 255) / 256, c->num_rows, digits), 256, 0, st>>>(kctx(c), kb, ka, (ulonglong2 *)out,
+                                                                                  digits, c->log_n);
+    }
+    LAUNCH_CHECK();
+    return HEB_OK;
 }
 
 // which = 0: aP = center_P(INTT_P(acc_P)) ; which = 1: bL = INTT_L(acc_L + P d_L) (std form)
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_ks_down_head(Ctx K, const u64 *acc, heb_ct d, int k,
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_down_head(Ctx K, const u64 *acc, heb_ct d, int k,
                                                                         i64 *aP, u64 *bL, int64_t count) {
     extern __shared__ u64 sm[];
     const int which = blockIdx.x, c = blockIdx.z;
@@ -193,7 +243,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_ks_down_head(Ctx K, con
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_ks_down_rescale_tail(Ctx K, const u64 *acc, heb_ct d,
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_down_rescale_tail(Ctx K, const u64 *acc, heb_ct d,
                                                                                 const i64 *aP, const u64 *bL, int k,
                                                                                 heb_ct out, int64_t count) {
     extern __shared__ u64 sm[];
@@ -235,7 +285,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_ks_down_rescale_tail(Ct
 
 // ModDown without rescale (rotation): out_i = acc_i P^-1 - NTT_i(aP P^-1 R) [+ add0_i for c = 0]
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_ks_down_tail(Ctx K, const u64 *acc, const i64 *aP, int k,
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_down_tail(Ctx K, const u64 *acc, const i64 *aP, int k,
                                                                         heb_ct add0, heb_ct out, int64_t count) {
     extern __shared__ u64 sm[];
     const int i = blockIdx.x, c = blockIdx.z;
@@ -263,7 +313,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_ks_down_tail(Ctx K, con
 }
 
 template <int LOGN>
-static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const u64 *kb, const u64 *ka, heb_ct d, heb_ct out,
+static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *key, heb_ct d, heb_ct out,
                             int64_t count, int level, bool rescale, cudaStream_t st) {
     constexpr int T = ntt::Shape<LOGN>::T;
     constexpr size_t sm = smem_bytes<LOGN>();
@@ -290,7 +340,7 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const u64 *kb, con
         const unsigned gy = gdim(cnt);
         { PROF("k_ks_head", st, 16.0 * n * cnt * k); k_ks_head<LOGN><<<dim3(k, gy), T, sm, st>>>(K, s, comp, (i64 *)sD.p, k, cnt); }
         LAUNCH_CHECK();
-        { PROF("k_ks_modup", st, 8.0 * n * (2.0 * cnt * k + 2.0 * k * (k + 1) + 2.0 * cnt * (k + 1))); k_ks_modup<LOGN><<<dim3(k + 1, gy), T, sm, st>>>(K, s, comp, (const i64 *)sD.p, kb, ka, k, (u64 *)sA.p, cnt); }
+        { PROF("k_ks_modup", st, 8.0 * n * (2.0 * cnt * k + 2.0 * k * (k + 1) + 2.0 * cnt * (k + 1))); k_ks_modup<LOGN><<<dim3(k + 1, gy), ntt::Shape<LOGN, MODUP_E(LOGN)>::T, sm, st>>>(K, s, comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt); }
         LAUNCH_CHECK();
         if (rescale) {
             { PROF("k_ks_down_head", st, 8.0 * n * cnt * 10.0); k_ks_down_head<LOGN><<<dim3(2, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
@@ -312,18 +362,19 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const u64 *kb, con
     return HEB_OK;
 }
 
-extern "C" int heb_relin_rescale(heb_ctx *c, heb_ct raw, const uint64_t *evk_b, const uint64_t *evk_a, heb_ct out,
-                                 int64_t count, int level, void *stream) {
-    if (!c || !evk_b || !evk_a || level < 1 || level > c->num_rows - 2)
+extern "C" int heb_relin_rescale(heb_ctx *c, heb_ct raw, const uint64_t *evk, heb_ct out, int64_t count, int level,
+                                 void *stream) {
+    if (!c || !evk || level < 1 || level > c->num_rows - 2)
         return fail(HEB_EINVAL, "heb_relin_rescale: bad level %d", level);
     if (count <= 0) return HEB_OK;
     // d2 = component 2 of raw; d0/d1 = components 0/1
-    DISPATCH_LOGN(c, launch_keyswitch, c, raw, 2, evk_b, evk_a, raw, out, count, level, true, (cudaStream_t)stream);
+    DISPATCH_LOGN(c, launch_keyswitch, c, raw, 2, (const ulonglong2 *)evk, raw, out, count, level, true,
+                  (cudaStream_t)stream);
 }
 
-extern "C" int heb_rotate(heb_ctx *c, heb_ct ct, const uint64_t *gk_b, const uint64_t *gk_a, heb_ct out,
-                          int64_t count, int level, uint64_t galois, void *stream) {
-    if (!c || !gk_b || !gk_a || level < 0 || level > c->num_rows - 2 || !(galois & 1))
+extern "C" int heb_rotate(heb_ctx *c, heb_ct ct, const uint64_t *gk, heb_ct out, int64_t count, int level,
+                          uint64_t galois, void *stream) {
+    if (!c || !gk || level < 0 || level > c->num_rows - 2 || !(galois & 1))
         return fail(HEB_EINVAL, "heb_rotate: bad args");
     if (count <= 0) return HEB_OK;
     cudaStream_t st = (cudaStream_t)stream;
@@ -335,6 +386,6 @@ extern "C" int heb_rotate(heb_ctx *c, heb_ct ct, const uint64_t *gk_b, const uin
     const int64_t lines = count * 2 * k;
     { PROF("k_galois_ct", st, 16.0 * c->n * lines); k_galois_ct<<<pw_grid(c->n, lines), 256, 0, st>>>(ct, r, lines, k, c->log_n, galois % (2ull * c->n)); }
     LAUNCH_CHECK();
-    DISPATCH_LOGN(c, launch_keyswitch, c, r, 1, gk_b, gk_a, r, out, count, level, false, st);
+    DISPATCH_LOGN(c, launch_keyswitch, c, r, 1, (const ulonglong2 *)gk, r, out, count, level, false, st);
 }
 

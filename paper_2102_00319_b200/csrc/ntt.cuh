@@ -8,16 +8,17 @@
 //            n^-1 folded into the last stage), so results are bit-identical to the
 //            reference's backwards table walk.
 //
-// Work split: one CTA of T = N/16 threads owns one row of N residues.  The n stages
-// are processed in register-blocked groups: a radix-2^r group gives each thread a
-// "unit" of 2^r elements that stay in registers for r stages; units exchange through
-// shared memory between groups (padded index i + i/16 keeps 64-bit accesses free of
-// bank conflicts for every group shape used here).  n = 4*G + REM gives G radix-16
-// groups plus one radix-2^REM group (first in forward order, last in inverse order).
+// Work split: one CTA of T = N/E threads owns one row of N residues (E = 8 or 16
+// elements per thread).  The n stages are processed in register-blocked groups: a
+// radix-2^r group gives each thread a "unit" of 2^r elements that stay in registers
+// for r stages; units exchange through shared memory between groups (padded index
+// i + i/16 keeps 64-bit accesses (nearly) free of bank conflicts).  n = e*G + REM
+// (E = 2^e) gives G radix-E groups plus one radix-2^REM group (first in forward
+// order, last in inverse order).
 //
 // Interfaces chosen so that callers can fuse prologues/epilogues:
 //   forward: input through a functor load(idx) (coalesced across threads), output
-//            left in registers: thread t holds positions [16t, 16t+16) of the result;
+//            left in registers: thread t holds positions [E t, E t + E) of the result;
 //   inverse: input given in registers in that same layout, output through a functor
 //            store(idx, value) (coalesced).
 // Lazy reduction: forward values live in [0, 4p), inverse values in [0, 2p); all
@@ -29,21 +30,23 @@ namespace ntt {
 
 HD int pad(int i) { return i + (i >> 4); }
 
-template <int LOGN>
+template <int LOGN, int E = 16>
 struct Shape {
+    static_assert(E == 8 || E == 16, "8 or 16 elements per thread");
+    static constexpr int LOGE = E == 8 ? 3 : 4;
     static constexpr int N = 1 << LOGN;
-    static constexpr int T = N / 16;
-    static constexpr int REM = LOGN % 4;
-    static constexpr int G = LOGN / 4;
+    static constexpr int T = N / E;
+    static constexpr int REM = LOGN % LOGE;
+    static constexpr int G = LOGN / LOGE;
     static constexpr int SMEM_WORDS = N + N / 16;
 };
 
 // ---------------------------------------------------------------- forward ----
 // One forward group: radix 2^RB covering stages S0 .. S0+RB-1.
 // SRC: 0 = functor load, 1 = shared memory.  DST: 0 = shared memory, 1 = registers.
-template <int LOGN, int RB, int S0, int SRC, int DST, class Load>
-HD void fwd_group(u64 *sm, const ulonglong2 *__restrict__ tw, u64 p, Load &load, u64 (&out)[16]) {
-    using S = Shape<LOGN>;
+template <int LOGN, int E, int RB, int S0, int SRC, int DST, class Load>
+HD void fwd_group(u64 *sm, const ulonglong2 *__restrict__ tw, u64 p, Load &load, u64 (&out)[E]) {
+    using S = Shape<LOGN, E>;
     constexpr int R = 1 << RB;
     constexpr int LB = LOGN - S0 - RB;
     constexpr int UPT = (S::N / R) / S::T;
@@ -76,7 +79,7 @@ HD void fwd_group(u64 *sm, const ulonglong2 *__restrict__ tw, u64 p, Load &load,
             }
         }
         if constexpr (DST == 1) {
-            static_assert(UPT == 1 && R == 16, "register output needs one radix-16 unit per thread");
+            static_assert(UPT == 1 && R == E, "register output needs one radix-E unit per thread");
 #pragma unroll
             for (int m = 0; m < R; ++m) out[m] = csub(csub(x[m], p2), p);
         } else {
@@ -86,39 +89,39 @@ HD void fwd_group(u64 *sm, const ulonglong2 *__restrict__ tw, u64 p, Load &load,
     }
 }
 
-template <int LOGN, int GI, class Load>
-HD void fwd_radix16_groups(u64 *sm, const ulonglong2 *__restrict__ tw, u64 p, Load &load, u64 (&out)[16]) {
-    using S = Shape<LOGN>;
-    constexpr int S0 = S::REM + 4 * GI;
+template <int LOGN, int E, int GI, class Load>
+HD void fwd_main_groups(u64 *sm, const ulonglong2 *__restrict__ tw, u64 p, Load &load, u64 (&out)[E]) {
+    using S = Shape<LOGN, E>;
+    constexpr int S0 = S::REM + S::LOGE * GI;
     constexpr bool first = (S0 == 0);
     constexpr bool last = (GI == S::G - 1);
-    fwd_group<LOGN, 4, S0, first ? 0 : 1, last ? 1 : 0>(sm, tw, p, load, out);
+    fwd_group<LOGN, E, S::LOGE, S0, first ? 0 : 1, last ? 1 : 0>(sm, tw, p, load, out);
     if constexpr (!last) {
         __syncthreads();
-        fwd_radix16_groups<LOGN, GI + 1>(sm, tw, p, load, out);
+        fwd_main_groups<LOGN, E, GI + 1>(sm, tw, p, load, out);
     }
 }
 
 // Forward NTT of one row.  `load(idx)` returns the input residue at natural position
-// idx (in [0, 2p)); on return thread t holds output positions 16t .. 16t+15.
-template <int LOGN, class Load>
-__device__ void forward(u64 *sm, const ulonglong2 *__restrict__ tw, u64 p, Load load, u64 (&out)[16]) {
-    using S = Shape<LOGN>;
+// idx (in [0, 2p)); on return thread t holds output positions E t .. E t + E - 1.
+template <int LOGN, int E = 16, class Load>
+__device__ void forward(u64 *sm, const ulonglong2 *__restrict__ tw, u64 p, Load load, u64 (&out)[E]) {
+    using S = Shape<LOGN, E>;
     static_assert(LOGN >= 6 && LOGN <= 14, "single-CTA engine covers N = 64 .. 16384");
     __syncthreads();  // shared memory may still be read by a previous transform
     if constexpr (S::REM) {
-        fwd_group<LOGN, S::REM, 0, 0, 0>(sm, tw, p, load, out);
+        fwd_group<LOGN, E, S::REM, 0, 0, 0>(sm, tw, p, load, out);
         __syncthreads();
     }
-    fwd_radix16_groups<LOGN, 0>(sm, tw, p, load, out);
+    fwd_main_groups<LOGN, E, 0>(sm, tw, p, load, out);
 }
 
 // ---------------------------------------------------------------- inverse ----
 // SRC: 1 = registers, 0 = shared memory.  DST: 0 = shared memory, 1 = functor store.
-template <int LOGN, int RB, int S0, int SRC, int DST, class Store>
-HD void inv_group(u64 *sm, const ulonglong2 *__restrict__ itw, u64 p, const u64 (&in)[16], Store &store,
+template <int LOGN, int E, int RB, int S0, int SRC, int DST, class Store>
+HD void inv_group(u64 *sm, const ulonglong2 *__restrict__ itw, u64 p, const u64 (&in)[E], Store &store,
                   ulonglong2 last_u, ulonglong2 last_v) {
-    using S = Shape<LOGN>;
+    using S = Shape<LOGN, E>;
     constexpr int R = 1 << RB;
     constexpr int LB = LOGN - S0 - RB;
     constexpr int UPT = (S::N / R) / S::T;
@@ -132,7 +135,7 @@ HD void inv_group(u64 *sm, const ulonglong2 *__restrict__ itw, u64 p, const u64 
         const int base = (uhigh << (LOGN - S0)) | ulow;
         u64 x[R];
         if constexpr (SRC == 1) {
-            static_assert(UPT == 1 && R == 16, "register input needs one radix-16 unit per thread");
+            static_assert(UPT == 1 && R == E, "register input needs one radix-E unit per thread");
 #pragma unroll
             for (int m = 0; m < R; ++m) x[m] = in[m];
         } else {
@@ -167,34 +170,34 @@ HD void inv_group(u64 *sm, const ulonglong2 *__restrict__ itw, u64 p, const u64 
     }
 }
 
-template <int LOGN, int GI, class Store>
-HD void inv_radix16_groups(u64 *sm, const ulonglong2 *__restrict__ itw, u64 p, const u64 (&in)[16], Store &store,
-                           ulonglong2 last_u, ulonglong2 last_v) {
+template <int LOGN, int E, int GI, class Store>
+HD void inv_main_groups(u64 *sm, const ulonglong2 *__restrict__ itw, u64 p, const u64 (&in)[E], Store &store,
+                        ulonglong2 last_u, ulonglong2 last_v) {
     // GI counts down from G-1 (first inverse group, register input) to 0.
-    using S = Shape<LOGN>;
-    constexpr int S0 = S::REM + 4 * GI;
+    using S = Shape<LOGN, E>;
+    constexpr int S0 = S::REM + S::LOGE * GI;
     constexpr bool first = (GI == S::G - 1);
     constexpr bool last = (S0 == 0);
-    inv_group<LOGN, 4, S0, first ? 1 : 0, last ? 1 : 0>(sm, itw, p, in, store, last_u, last_v);
+    inv_group<LOGN, E, S::LOGE, S0, first ? 1 : 0, last ? 1 : 0>(sm, itw, p, in, store, last_u, last_v);
     if constexpr (GI > 0) {
         __syncthreads();
-        inv_radix16_groups<LOGN, GI - 1>(sm, itw, p, in, store, last_u, last_v);
+        inv_main_groups<LOGN, E, GI - 1>(sm, itw, p, in, store, last_u, last_v);
     }
 }
 
-// Inverse NTT of one row.  Thread t supplies positions 16t .. 16t+15 (values in
+// Inverse NTT of one row.  Thread t supplies positions E t .. E t + E - 1 (values in
 // [0, 2p)); results leave through store(idx, canonical value).  last_u = n^-1 * c and
 // last_v = itw[1] * n^-1 * c (Shoup pairs) for a caller-chosen output factor c.
-template <int LOGN, class Store>
-__device__ void inverse(u64 *sm, const ulonglong2 *__restrict__ itw, u64 p, const u64 (&in)[16], Store store,
+template <int LOGN, int E = 16, class Store>
+__device__ void inverse(u64 *sm, const ulonglong2 *__restrict__ itw, u64 p, const u64 (&in)[E], Store store,
                         ulonglong2 last_u, ulonglong2 last_v) {
-    using S = Shape<LOGN>;
+    using S = Shape<LOGN, E>;
     static_assert(LOGN >= 6 && LOGN <= 14, "single-CTA engine covers N = 64 .. 16384");
     __syncthreads();
-    inv_radix16_groups<LOGN, S::G - 1>(sm, itw, p, in, store, last_u, last_v);
+    inv_main_groups<LOGN, E, S::G - 1>(sm, itw, p, in, store, last_u, last_v);
     if constexpr (S::REM) {
         __syncthreads();
-        inv_group<LOGN, S::REM, 0, 0, 1>(sm, itw, p, in, store, last_u, last_v);
+        inv_group<LOGN, E, S::REM, 0, 0, 1>(sm, itw, p, in, store, last_u, last_v);
     }
 }
 

@@ -5,7 +5,7 @@
 // transforms
 // =============================================================================
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_ntt_fwd(Ctx K, u64 *data, int64_t count, int row0,
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ntt_fwd(Ctx K, u64 *data, int64_t count, int row0,
                                                                    int64_t bstride) {
     extern __shared__ u64 sm[];
     const int r = blockIdx.x, prime = row0 + r;
@@ -20,7 +20,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_ntt_fwd(Ctx K, u64 *dat
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_ntt_inv(Ctx K, u64 *data, int64_t count, int row0,
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ntt_inv(Ctx K, u64 *data, int64_t count, int row0,
                                                                    int64_t bstride) {
     extern __shared__ u64 sm[];
     const int r = blockIdx.x, prime = row0 + r;
@@ -67,7 +67,7 @@ extern "C" int heb_ntt_inv(heb_ctx *c, uint64_t *data, int64_t count, int rows, 
 
 // spread_centered + ntt_fwd_rows (ckks.py:120-126): signed coefficient -> (v mod p) * R, NTT
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_spread_ntt(Ctx K, const i64 *coeffs, int64_t count,
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_spread_ntt(Ctx K, const i64 *coeffs, int64_t count,
                                                                       u64 *out, int64_t ostride) {
     extern __shared__ u64 sm[];
     const int r = blockIdx.x;
@@ -102,7 +102,7 @@ extern "C" int heb_spread_ntt(heb_ctx *c, const int64_t *coeffs, int64_t count, 
 // client side: encrypt / decrypt / key generation (ckks.py:135-273)
 // =============================================================================
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_encrypt(Ctx K, const i64 *v, const i64 *e0m, const i64 *e1,
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_encrypt(Ctx K, const i64 *v, const i64 *e0m, const i64 *e1,
                                                                    const u64 *pkb, const u64 *pka, heb_ct out,
                                                                    int64_t count) {
     extern __shared__ u64 sm[];
@@ -147,7 +147,7 @@ extern "C" int heb_encrypt(heb_ctx *c, const int64_t *v, const int64_t *e0m, con
 
 // decrypt rows 0/1: m = c1*s + c0 -> INTT -> std form
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_decrypt_rows(Ctx K, heb_ct ct, const u64 *s, u64 *tmp,
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_decrypt_rows(Ctx K, heb_ct ct, const u64 *s, u64 *tmp,
                                                                         int rows, int64_t count) {
     extern __shared__ u64 sm[];
     const int r = blockIdx.x;
@@ -214,7 +214,7 @@ extern "C" int heb_decrypt(heb_ctx *c, heb_ct ct, const uint64_t *s_eval, int64_
 
 // pk_b = e - a*s   (row r)
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_make_pk(Ctx K, const u64 *s, const u64 *a, const i64 *e,
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_make_pk(Ctx K, const u64 *s, const u64 *a, const i64 *e,
                                                                    u64 *pkb) {
     extern __shared__ u64 sm[];
     const int r = blockIdx.x;
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_make_pk(Ctx K, const u6
 
 // kb[j][r] = e_j - a_j,r s_r  (+ (P mod q_j) R * target_j on r == j, applied with mont_mul)
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T) k_make_swk(Ctx K, const u64 *s, const u64 *target,
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_make_swk(Ctx K, const u64 *s, const u64 *target,
                                                                     const u64 *a, const i64 *e, u64 *kb) {
     extern __shared__ u64 sm[];
     const int r = blockIdx.x, j = blockIdx.y;

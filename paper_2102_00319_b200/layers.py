@@ -135,7 +135,7 @@ class LayerEvaluator:
         evk = self.be._require_eval_key().evaluation
         n_out = raw.shape[0]
         out = self._empty(n_out, 2, level)
-        self.ctx.call("heb_relin_rescale", ct_desc(raw), evk.b.data_ptr(), evk.a.data_ptr(), ct_desc(out), n_out, level,
+        self.ctx.call("heb_relin_rescale", ct_desc(raw), evk.prep.data_ptr(), ct_desc(out), n_out, level,
                       self.ctx.stream)
         new_scale = self.be._rescale_scale(scale, level)
         return CipherBatch(out, level - 1, new_scale, max(noise, self.be._round_noise_bits(new_scale)))
