@@ -139,6 +139,12 @@ int heb_make_switch_key(heb_ctx *ctx, const uint64_t *s_eval, const uint64_t *ta
  * (degree-2 tensor, lazy 128-bit accumulation); index arrays are device int32. */
 int heb_dot_tensor(heb_ctx *ctx, heb_ct a, heb_ct b, const int32_t *a_idx, const int32_t *b_idx, int taps,
                    heb_ct raw, int64_t n_out, int k, void *stream);
+/* Convolution layer tensor (layers.py:92-127 fused): A holds channels*m*n input cells
+ * (item = c*m*n + i*n + j), B the broadcast weights (item = ((f*channels + c)*kp + p)*kq
+ * + q); raw output item f*om*on + i*on + j = sum over (c,p,q) of A (x) B for a valid,
+ * `stride`d cross-correlation.  Weights are staged in shared memory per position tile. */
+int heb_conv_tensor(heb_ctx *ctx, heb_ct a, heb_ct b, heb_ct raw, int channels, int m, int n, int filters, int kp,
+                    int kq, int stride, int k, void *stream);
 /* out_o = sum_{t<terms} A[idx[o*terms+t]] over `comps` components (pool windows). */
 int heb_sum_gather(heb_ctx *ctx, heb_ct a, const int32_t *idx, int terms, heb_ct out, int64_t n_out, int comps,
                    int k, void *stream);

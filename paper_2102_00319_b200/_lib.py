@@ -58,6 +58,7 @@ SIGNATURES: dict[str, list] = {
     "heb_make_public_key": [_P, _P, _P, _P, _P, _I, _P],
     "heb_make_switch_key": [_P, _P, _P, _P, _P, _P, _I, _P],
     "heb_dot_tensor": [_P, _CT, _CT, _P, _P, _I, _CT, _L, _I, _P],
+    "heb_conv_tensor": [_P, _CT, _CT, _CT, _I, _I, _I, _I, _I, _I, _I, _I, _P],
     "heb_sum_gather": [_P, _CT, _P, _I, _CT, _L, _I, _I, _P],
     "heb_gather": [_P, _CT, _P, _CT, _L, _I, _I, _P],
     "heb_prof_enable": [_I],

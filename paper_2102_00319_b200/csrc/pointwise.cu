@@ -166,7 +166,7 @@ __global__ void k_dot_tensor(Ctx K, heb_ct A, heb_ct B, const int32_t *ia, const
     const int r = blockIdx.z;
     const PrimeInfo P = K.pi[r];
     for (int64_t o = blockIdx.y; o < n_out; o += gridDim.y) {
-        acc128 s0 = {0, 0}, s1 = {0, 0}, s2 = {0, 0};
+        acc4 s0 = {0, 0, 0, 0}, s1 = {0, 0, 0, 0}, s2 = {0, 0, 0, 0};
         u64 t0 = 0, t1 = 0, t2 = 0;
         int since = 0;
         for (int t = 0; t < taps; ++t) {
@@ -175,20 +175,20 @@ __global__ void k_dot_tensor(Ctx K, heb_ct A, heb_ct B, const int32_t *ia, const
             const u64 *bp = B.data + b * B.ct_stride + ((int64_t)r << logn) + x;
             const u64 a0 = __ldg(ap), a1 = __ldg(ap + A.comp_stride);
             const u64 b0 = __ldg(bp), b1 = __ldg(bp + B.comp_stride);
-            mac(s0, a0, b0);
-            mac(s2, a1, b1);
-            mac(s1, add_mod(a0, a1, P.p), add_mod(b0, b1, P.p));
+            mac4(s0, a0, b0);
+            mac4(s2, a1, b1);
+            mac4(s1, add_mod(a0, a1, P.p), add_mod(b0, b1, P.p));
             if (++since == flush) {
-                t0 = add_mod(t0, redc128(s0, P.p, P.pinv, P.r1s), P.p);
-                t1 = add_mod(t1, redc128(s1, P.p, P.pinv, P.r1s), P.p);
-                t2 = add_mod(t2, redc128(s2, P.p, P.pinv, P.r1s), P.p);
-                s0 = s1 = s2 = acc128{0, 0};
+                t0 = add_mod(t0, redc128(to128(s0), P.p, P.pinv, P.r1s), P.p);
+                t1 = add_mod(t1, redc128(to128(s1), P.p, P.pinv, P.r1s), P.p);
+                t2 = add_mod(t2, redc128(to128(s2), P.p, P.pinv, P.r1s), P.p);
+                s0 = s1 = s2 = acc4{0, 0, 0, 0};
                 since = 0;
             }
         }
-        t0 = add_mod(t0, redc128(s0, P.p, P.pinv, P.r1s), P.p);
-        t1 = add_mod(t1, redc128(s1, P.p, P.pinv, P.r1s), P.p);
-        t2 = add_mod(t2, redc128(s2, P.p, P.pinv, P.r1s), P.p);
+        t0 = add_mod(t0, redc128(to128(s0), P.p, P.pinv, P.r1s), P.p);
+        t1 = add_mod(t1, redc128(to128(s1), P.p, P.pinv, P.r1s), P.p);
+        t2 = add_mod(t2, redc128(to128(s2), P.p, P.pinv, P.r1s), P.p);
         u64 *dp = D.data + o * D.ct_stride + ((int64_t)r << logn) + x;
         dp[0] = t0;
         dp[D.comp_stride] = sub_mod(sub_mod(t1, t0, P.p), t2, P.p);

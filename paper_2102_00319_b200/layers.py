@@ -91,9 +91,10 @@ def drop_batch(b: CipherBatch, level: int) -> CipherBatch:
 class LayerEvaluator:
     """Runs an ``EncryptedNetworkBatch`` over a packed input batch on one device."""
 
-    def __init__(self, backend: B200Backend):
+    def __init__(self, backend: B200Backend, fused_conv: bool = True):
         self.be = backend
         self.ctx = backend.ctx
+        self.fused_conv = fused_conv
         self._idx_cache: dict = {}
         self._unique: dict = {}
 
@@ -130,6 +131,23 @@ class LayerEvaluator:
         noise = term + math.log2(taps) if term > float("-inf") else term
         self.be.counters.bump(ctct_mult=n_out * taps, ctct_add=n_out * (taps - 1))
         return raw, lvl, a.scale * b.scale, noise
+
+    def conv_dot(self, a: CipherBatch, w: CipherBatch, c_in: int, m: int, n: int, layer: Conv, n_out: int, taps: int):
+        """Fused convolution tensor (heb_conv_tensor): weights staged in shared memory."""
+        lvl = min(a.level, w.level)
+        if lvl < 1:
+            raise DepthExhausted("ciphertext-ciphertext multiply at level 0")
+        k = lvl + 1
+        raw = self._empty(n_out, 3, k)
+        p, q = layer.kernel
+        self.ctx.call("heb_conv_tensor", a.desc(), w.desc(), ct_desc(raw), c_in, m, n, layer.filters, p, q,
+                      layer.stride, k, self.ctx.stream)
+        term = noise_sum(a.noise_bits, w.noise_bits)
+        if term > float("-inf"):
+            term += 1.0
+        noise = term + math.log2(taps) if term > float("-inf") else term
+        self.be.counters.bump(ctct_mult=n_out * taps, ctct_add=n_out * (taps - 1))
+        return raw, lvl, a.scale * w.scale, noise
 
     def finalize(self, raw: torch.Tensor, level: int, scale: Fraction, noise: float) -> CipherBatch:
         evk = self.be._require_eval_key().evaluation
@@ -207,8 +225,11 @@ class LayerEvaluator:
             ib = ((f * c_in + c) * p + dp) * q + dq
             return np.stack([ia.reshape(n_out, taps), ib.reshape(n_out, taps)])
 
-        idx = self._idx(("conv", dims, layer.kernel, s, F), build)
-        raw, lvl, scale, noise = self.dot(x, w, idx[0], idx[1], taps, n_out)
+        if self.fused_conv and taps <= 64:
+            raw, lvl, scale, noise = self.conv_dot(x, w, c_in, m, n, layer, n_out, taps)
+        else:
+            idx = self._idx(("conv", dims, layer.kernel, s, F), build)
+            raw, lvl, scale, noise = self.dot(x, w, idx[0], idx[1], taps, n_out)
         y = self.finalize(raw, lvl, scale, noise)
         if bias is not None:
             for f in range(F):

@@ -195,10 +195,12 @@ def test_cfg1_digests_match_reference(golden):
         assert list(be.decrypt(mul, keys).values[:8]) == rec["mul_dec8"]
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("name", ["mini2", "mini3", "mini4"])
-def test_batched_layers_match_reference(golden, dev_s128, name):
+def test_batched_layers_match_reference(golden, dev_s128, name, fused):
     """The batched layer evaluator (one launch sequence per layer) reproduces the
-    reference op sequence bit for bit, including levels, scales and counters."""
+    reference op sequence bit for bit, including levels, scales and counters --
+    with the fused convolution kernel and with the generic gather-dot path."""
     from nets import mini_networks
     from paper_2102_00319_b200 import layers
 
@@ -209,7 +211,7 @@ def test_batched_layers_match_reference(golden, dev_s128, name):
     enc = layers.encrypt_network(be, net, keys)
     be.counters.reset()
     x = layers.encrypt_images(be, imgs, keys)
-    out = layers.LayerEvaluator(be).run(enc, x)
+    out = layers.LayerEvaluator(be, fused_conv=fused).run(enc, x)
     g = golden["minis"][name]
     digests = [digest(np.concatenate(be.cipher_rows_host(be.batch_to_cipher(out, i)))) for i in range(out.count)]
     assert digests == g["logit_digests"]
