@@ -14,7 +14,7 @@ import threading
 from .errors import ConfigurationError, DeviceError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libheb200.so")
+LIB_PATH = os.environ.get("HEB_LIB_PATH") or os.path.join(HERE, "libheb200.so")
 
 
 class HebCt(ctypes.Structure):

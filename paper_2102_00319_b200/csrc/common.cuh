@@ -60,9 +60,10 @@ struct LevelConst {
     ulonglong2 pmod, pinv;       // P mod q_i, P^-1 mod q_i       (std)
 };
 
-struct LastConst {  // final inverse-stage factors (Shoup pairs)
+struct LastConst {  // final inverse-stage factors (Shoup pairs; FP64 engine: (w, w/p))
     ulonglong2 u_plain, v_plain;  // n^-1,       itw[1] n^-1
     ulonglong2 u_std, v_std;      // n^-1 R^-1,  itw[1] n^-1 R^-1  (fold from-Montgomery)
+    double2 fu_plain, fv_plain, fu_std, fv_std;
 };
 
 struct heb_ctx {
@@ -70,6 +71,7 @@ struct heb_ctx {
     std::vector<u64> primes;
     PrimeInfo *d_pi = nullptr;
     ulonglong2 *d_tw = nullptr, *d_itw = nullptr;
+    double2 *d_twf = nullptr, *d_itwf = nullptr;  // FP64 engine tables (w, w/p)
     LevelConst *d_lc = nullptr;
     LastConst *d_last = nullptr;
     int flush = 64;  // lazy 128-bit accumulation: products summed before a reduction
@@ -92,11 +94,39 @@ struct Scratch {
 struct Ctx {  // kernel-side view of the context
     const PrimeInfo *pi;
     const ulonglong2 *tw, *itw;
+    const double2 *twf, *itwf;
     const LevelConst *lc;
     const LastConst *last;
     int num_rows;
 };
-static inline Ctx kctx(const heb_ctx *c) { return Ctx{c->d_pi, c->d_tw, c->d_itw, c->d_lc, c->d_last, c->num_rows}; }
+static inline Ctx kctx(const heb_ctx *c) {
+    return Ctx{c->d_pi, c->d_tw, c->d_itw, c->d_twf, c->d_itwf, c->d_lc, c->d_last, c->num_rows};
+}
+
+// Row-dispatched transforms: rows whose prime is < 2^42 run on the FP64 engine, the
+// others (50/60-bit base and special primes) on the 64-bit integer engine.  Both read
+// u64 residues and return canonical u64 residues, so callers are engine-agnostic.
+template <int LOGN, int E = 16, class Load>
+__device__ __forceinline__ void fwd_any(const Ctx &K, int row, const PrimeInfo &P, u64 *sm, Load load,
+                                        u64 (&out)[E]) {
+    if (P.use_fp)
+        ntt::forward_fp<LOGN, E>(reinterpret_cast<double *>(sm), K.twf + ((size_t)row << LOGN), P.pd, P.pinvd, load,
+                                 out);
+    else
+        ntt::forward<LOGN, E>(sm, K.tw + ((size_t)row << LOGN), P.p, load, out);
+}
+// std_out: fold the from-Montgomery factor R^-1 into the final stage
+template <int LOGN, int E = 16, class Store>
+__device__ __forceinline__ void inv_any(const Ctx &K, int row, const PrimeInfo &P, u64 *sm, const u64 (&in)[E],
+                                        Store store, bool std_out) {
+    const LastConst &lc = K.last[row];
+    if (P.use_fp)
+        ntt::inverse_fp<LOGN, E>(reinterpret_cast<double *>(sm), K.itwf + ((size_t)row << LOGN), P.pd, P.pinvd, in,
+                                 store, std_out ? lc.fu_std : lc.fu_plain, std_out ? lc.fv_std : lc.fv_plain);
+    else
+        ntt::inverse<LOGN, E>(sm, K.itw + ((size_t)row << LOGN), P.p, in, store, std_out ? lc.u_std : lc.u_plain,
+                              std_out ? lc.v_std : lc.v_plain);
+}
 
 template <int LOGN>
 __device__ __forceinline__ const ulonglong2 *tw_row(const Ctx &k, int row) {
@@ -124,7 +154,11 @@ __device__ __forceinline__ void store16(u64 *__restrict__ dst, const u64 (&v)[16
 }
 
 // minimum resident CTAs per SM for the NTT kernels: caps registers at 64/thread
-#define NTT_MINB(LOGN) ((1024 >> ((LOGN) - 4)) > 32 ? 32 : (1024 >> ((LOGN) - 4)))
+#ifndef NTT_REGS_PER_THREAD
+#define NTT_REGS_PER_THREAD 64
+#endif
+#define NTT_MINB(LOGN) \
+    (((65536 / NTT_REGS_PER_THREAD) >> ((LOGN) - 4)) > 32 ? 32 : (((65536 / NTT_REGS_PER_THREAD) >> ((LOGN) - 4)) < 1 ? 1 : ((65536 / NTT_REGS_PER_THREAD) >> ((LOGN) - 4))))
 
 template <int LOGN>
 static constexpr size_t smem_bytes() {

@@ -89,7 +89,10 @@ extern "C" int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows
     }
     std::vector<PrimeInfo> pi(num_rows);
     std::vector<ulonglong2> tw((size_t)num_rows * n), itw((size_t)num_rows * n);
+    std::vector<double2> twf((size_t)num_rows * n), itwf((size_t)num_rows * n);
     std::vector<LastConst> last(num_rows);
+    const char *fp_env = getenv("HEB_DISABLE_FP64_NTT");
+    const bool fp_disabled = fp_env && fp_env[0] == '1';
     for (int r = 0; r < num_rows; ++r) {
         const u64 p = c->primes[r];
         const u64 g = psi ? psi[r] : find_2n_root_h(n, p);
@@ -124,6 +127,19 @@ extern "C" int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows
         last[r].v_plain = shoup_pair(mulmod_h(it1, q.ninv, p), p);
         last[r].u_std = shoup_pair(q.ninv_rinv, p);
         last[r].v_std = shoup_pair(mulmod_h(it1, q.ninv_rinv, p), p);
+        // FP64 engine (p < 2^42): doubles (w, w/p) for every twiddle / final-stage factor
+        q.pd = (double)p;
+        q.pinvd = 1.0 / (double)p;
+        q.use_fp = (p < (1ull << 42)) && !fp_disabled;
+        auto fpair = [&](u64 w) { return make_double2((double)w, (double)w / (double)p); };
+        for (int i = 0; i < n; ++i) {
+            twf[(size_t)r * n + i] = fpair(tw[(size_t)r * n + i].x);
+            itwf[(size_t)r * n + i] = fpair(itw[(size_t)r * n + i].x);
+        }
+        last[r].fu_plain = fpair(last[r].u_plain.x);
+        last[r].fv_plain = fpair(last[r].v_plain.x);
+        last[r].fu_std = fpair(last[r].u_std.x);
+        last[r].fv_std = fpair(last[r].v_std.x);
     }
     // per-level constants; P = special prime (last row)
     const int levels = num_rows - 1;  // level 0 .. num_rows-2
@@ -156,6 +172,10 @@ extern "C" int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows
         (e = cudaMalloc(&c->d_pi, sizeof(PrimeInfo) * num_rows)) != cudaSuccess ||
         (e = cudaMalloc(&c->d_tw, sizeof(ulonglong2) * tw.size())) != cudaSuccess ||
         (e = cudaMalloc(&c->d_itw, sizeof(ulonglong2) * itw.size())) != cudaSuccess ||
+        (e = cudaMalloc(&c->d_twf, sizeof(double2) * twf.size())) != cudaSuccess ||
+        (e = cudaMalloc(&c->d_itwf, sizeof(double2) * itwf.size())) != cudaSuccess ||
+        (e = cudaMemcpy(c->d_twf, twf.data(), sizeof(double2) * twf.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(c->d_itwf, itwf.data(), sizeof(double2) * itwf.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
         (e = cudaMalloc(&c->d_lc, sizeof(LevelConst) * lc.size())) != cudaSuccess ||
         (e = cudaMalloc(&c->d_last, sizeof(LastConst) * num_rows)) != cudaSuccess ||
         (e = cudaMemcpy(c->d_pi, pi.data(), sizeof(PrimeInfo) * num_rows, cudaMemcpyHostToDevice)) != cudaSuccess ||
@@ -166,6 +186,14 @@ extern "C" int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows
         heb_ctx_destroy(c);
         return fail(HEB_ECUDA, "context upload failed: %s", cudaGetErrorString(e));
     }
+    // Keep freed stream-ordered scratch in the pool: without a release threshold the
+    // key-switch intermediates (hundreds of MB per layer) are unmapped and remapped
+    // around every synchronisation.
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     *out = c;
     return HEB_OK;
 }
@@ -175,6 +203,8 @@ extern "C" int heb_ctx_destroy(heb_ctx *c) {
     cudaFree(c->d_pi);
     cudaFree(c->d_tw);
     cudaFree(c->d_itw);
+    cudaFree(c->d_twf);
+    cudaFree(c->d_itwf);
     cudaFree(c->d_lc);
     cudaFree(c->d_last);
     delete c;

@@ -24,8 +24,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_rescale
             for (int m = 0; m < 16; ++m) x[m] = mont_mul(x[m], y[m], P.p, P.pinv);
         }
         i64 *dst = V + (b * comps + c) * (1 << LOGN);
-        ntt::inverse<LOGN>(sm, itw_row<LOGN>(K, L), P.p, x, [&](int i, u64 v) { dst[i] = center(v, P.p); },
-                           lc.u_std, lc.v_std);
+        inv_any<LOGN>(K, L, P, sm, x, [&](int i, u64 v) { dst[i] = center(v, P.p); }, true);
     }
 }
 
@@ -40,7 +39,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_rescale
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         const i64 *src = V + (b * comps + c) * (1 << LOGN);
         u64 y[16];
-        ntt::forward<LOGN>(sm, tw_row<LOGN>(K, i), P.p,
+        fwd_any<LOGN>(K, i, P, sm,
                            [&](int j) { return signed_mul_const(src[j], C.beta_r.x, C.beta_r.y, P.p); }, y);
         u64 x[16];
         load16(at(in, b, c, i, LOGN) + threadIdx.x * 16, x);
@@ -114,8 +113,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_head
         u64 x[16];
         load16(at(src, b, comp, j, LOGN) + threadIdx.x * 16, x);
         i64 *dst = D + (b * k + j) * (1 << LOGN);
-        ntt::inverse<LOGN>(sm, itw_row<LOGN>(K, j), P.p, x, [&](int i, u64 v) { dst[i] = center(v, P.p); },
-                           lc.u_std, lc.v_std);
+        inv_any<LOGN>(K, j, P, sm, x, [&](int i, u64 v) { dst[i] = center(v, P.p); }, true);
     }
 }
 
@@ -153,7 +151,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN, MODUP_E(LOGN)>::T, MODUP_MINB
                 for (int m = 0; m < E; ++m) dig[m] = s[m];
             } else {
                 const i64 *dj = D + (b * k + j) * n;
-                ntt::forward<LOGN, E>(sm, tw_row<LOGN>(K, gt), P.p,
+                fwd_any<LOGN, E>(K, gt, P, sm,
                                       [&](int i) { return signed_mul_const(dj[i], P.rmod, P.rmod_s, P.p); }, dig);
             }
             const ulonglong2 *kb = key + (((size_t)j * K.num_rows + gt) * 2) * n + pos;
@@ -232,12 +230,10 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_down
 #pragma unroll
             for (int m = 0; m < 16; ++m) x[m] = add_mod(x[m], shoup(y[m], C.pmod.x, C.pmod.y, P.p), P.p);
             u64 *dst = bL + (b * 2 + c) * n;
-            ntt::inverse<LOGN>(sm, itw_row<LOGN>(K, row), P.p, x, [&](int i, u64 v) { dst[i] = v; }, lc.u_std,
-                               lc.v_std);
+            inv_any<LOGN>(K, row, P, sm, x, [&](int i, u64 v) { dst[i] = v; }, true);
         } else {
             i64 *dst = aP + (b * 2 + c) * n;
-            ntt::inverse<LOGN>(sm, itw_row<LOGN>(K, row), P.p, x, [&](int i, u64 v) { dst[i] = center(v, P.p); },
-                               lc.u_std, lc.v_std);
+            inv_any<LOGN>(K, row, P, sm, x, [&](int i, u64 v) { dst[i] = center(v, P.p); }, true);
         }
     }
 }
@@ -259,8 +255,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_down
         const i64 *ap = aP + (b * 2 + c) * n;
         const u64 *bl = bL + (b * 2 + c) * n;
         u64 y[16];
-        ntt::forward<LOGN>(
-            sm, tw_row<LOGN>(K, i), Pi.p,
+        fwd_any<LOGN>(K, i, Pi, sm,
             [&](int j) {
                 const i64 a = ap[j];
                 // s_L = (bL - aP) * P^-1 mod q_L, centred
@@ -296,7 +291,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_down
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         const i64 *ap = aP + (b * 2 + c) * n;
         u64 y[16];
-        ntt::forward<LOGN>(sm, tw_row<LOGN>(K, i), Pi.p,
+        fwd_any<LOGN>(K, i, Pi, sm,
                            [&](int j) { return signed_mul_const(ap[j], Ci.gamma_r.x, Ci.gamma_r.y, Pi.p); }, y);
         u64 x[16];
         load16(acc + ((b * 2 + c) * (k + 1) + i) * n + pos, x);

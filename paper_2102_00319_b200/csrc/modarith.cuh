@@ -101,6 +101,8 @@ struct PrimeInfo {
     u64 rinv, rinv_s;        // R^-1 mod p  (Montgomery -> std)
     u64 ninv, ninv_s;        // n^-1 mod p
     u64 ninv_rinv, ninv_rinv_s;  // n^-1 * R^-1 mod p  (INTT + from-Montgomery)
-    u64 pad[5];
+    double pd, pinvd;            // p and 1/p as doubles (FP64 engine)
+    u64 use_fp;                  // 1 if p < 2^42: NTTs of this row run on the FP64 pipe
+    u64 pad[2];
 };
 

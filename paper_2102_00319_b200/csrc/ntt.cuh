@@ -201,4 +201,191 @@ __device__ void inverse(u64 *sm, const ulonglong2 *__restrict__ itw, u64 p, cons
     }
 }
 
+// =============================================================================
+// FP64 engine for primes p < 2^42 (the 40-bit level primes).
+//
+// On sm_100a the DFMA pipe sustains the same 64 op/clk/SM as 32-bit IMAD, while a
+// 64-bit Shoup product costs ~8 IMAD-pipe issue slots (tools/pipes_bench.cu).  With
+// p < 2^42 residues are exact doubles and a product modulo p needs 6 FP64 ops:
+//     h = y*w;  l = fma(y, w, -h)            (y*w = h + l exactly)
+//     q = rint(y * (w/p))                    (fma with the 1.5*2^52 magic constant)
+//     r = fma(-q, p, h) + l                  (exact; r in (-p, 2p))
+// Values are kept *unreduced and signed* between stages: a forward stage adds at most
+// 2p in magnitude, the inverse's sum path doubles and is re-centred at every group
+// boundary, so everything stays below 2^47 and every step above stays exact.  Inputs
+// and outputs are canonical u64 residues, bit-identical to the integer engine.
+// =============================================================================
+#define FP_MAGIC 6755399441055744.0  // 1.5 * 2^52
+
+HD double u2d(u64 v) { return __longlong_as_double((long long)(0x4330000000000000ull | v)) - 4503599627370496.0; }
+HD double rint_fp(double x) { return (x + FP_MAGIC) - FP_MAGIC; }
+// y * w mod p, result in (-p, 2p); w2 = (w, w/p)
+HD double fmul(double y, double2 w2, double p) {
+    const double h = __dmul_rn(y, w2.x);
+    const double l = fma(y, w2.x, -h);
+    const double q = __dsub_rn(fma(y, w2.y, FP_MAGIC), FP_MAGIC);
+    return __dadd_rn(fma(-q, p, h), l);
+}
+// any |x| < 2^50 -> centred representative in about (-p/2, p/2]
+HD double fred(double x, double p, double pinv) {
+    const double q = __dsub_rn(fma(x, pinv, FP_MAGIC), FP_MAGIC);
+    return fma(-q, p, x);
+}
+// exact canonical residue in [0, p) as u64
+HD u64 fcanon(double x, double p, double pinv) {
+    double r = fred(x, p, pinv);
+    r = r < 0.0 ? r + p : r;
+    r = r >= p ? r - p : r;
+    return (u64)__double_as_longlong(r + 4503599627370496.0) & 0x000FFFFFFFFFFFFFull;
+}
+
+template <int LOGN, int E, int RB, int S0, int SRC, int DST, class Load>
+HD void fwd_group_fp(double *sm, const double2 *__restrict__ tw, double p, double pinv, Load &load,
+                     u64 (&out)[E]) {
+    using S = Shape<LOGN, E>;
+    constexpr int R = 1 << RB;
+    constexpr int LB = LOGN - S0 - RB;
+    constexpr int UPT = (S::N / R) / S::T;
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < UPT; ++k) {
+        const int u = tid + k * S::T;
+        const int ulow = u & ((1 << LB) - 1);
+        const int uhigh = u >> LB;
+        const int base = (uhigh << (LOGN - S0)) | ulow;
+        double x[R];
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            const int idx = base + (m << LB);
+            if constexpr (SRC == 0) x[m] = u2d(load(idx));
+            else x[m] = sm[pad(idx)];
+        }
+#pragma unroll
+        for (int q = 0; q < RB; ++q) {
+            const int half = R >> (q + 1);
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                if (m & half) continue;
+                const double2 w = tw[(1 << (S0 + q)) + (uhigh << q) + (m >> (RB - q))];
+                const double r = fmul(x[m + half], w, p);
+                x[m + half] = x[m] - r;
+                x[m] = x[m] + r;
+            }
+        }
+        if constexpr (DST == 1) {
+            static_assert(UPT == 1 && R == E, "register output needs one radix-E unit per thread");
+#pragma unroll
+            for (int m = 0; m < R; ++m) out[m] = fcanon(x[m], p, pinv);
+        } else {
+#pragma unroll
+            for (int m = 0; m < R; ++m) sm[pad(base + (m << LB))] = x[m];
+        }
+    }
+}
+
+template <int LOGN, int E, int GI, class Load>
+HD void fwd_main_groups_fp(double *sm, const double2 *__restrict__ tw, double p, double pinv, Load &load,
+                           u64 (&out)[E]) {
+    using S = Shape<LOGN, E>;
+    constexpr int S0 = S::REM + S::LOGE * GI;
+    constexpr bool first = (S0 == 0);
+    constexpr bool last = (GI == S::G - 1);
+    fwd_group_fp<LOGN, E, S::LOGE, S0, first ? 0 : 1, last ? 1 : 0>(sm, tw, p, pinv, load, out);
+    if constexpr (!last) {
+        __syncthreads();
+        fwd_main_groups_fp<LOGN, E, GI + 1>(sm, tw, p, pinv, load, out);
+    }
+}
+
+template <int LOGN, int E = 16, class Load>
+__device__ void forward_fp(double *sm, const double2 *__restrict__ tw, double p, double pinv, Load load,
+                           u64 (&out)[E]) {
+    using S = Shape<LOGN, E>;
+    static_assert(LOGN >= 6 && LOGN <= 14, "single-CTA engine covers N = 64 .. 16384");
+    __syncthreads();
+    if constexpr (S::REM) {
+        fwd_group_fp<LOGN, E, S::REM, 0, 0, 0>(sm, tw, p, pinv, load, out);
+        __syncthreads();
+    }
+    fwd_main_groups_fp<LOGN, E, 0>(sm, tw, p, pinv, load, out);
+}
+
+template <int LOGN, int E, int RB, int S0, int SRC, int DST, class Store>
+HD void inv_group_fp(double *sm, const double2 *__restrict__ itw, double p, double pinv, const u64 (&in)[E],
+                     Store &store, double2 last_u, double2 last_v) {
+    using S = Shape<LOGN, E>;
+    constexpr int R = 1 << RB;
+    constexpr int LB = LOGN - S0 - RB;
+    constexpr int UPT = (S::N / R) / S::T;
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < UPT; ++k) {
+        const int u = tid + k * S::T;
+        const int ulow = u & ((1 << LB) - 1);
+        const int uhigh = u >> LB;
+        const int base = (uhigh << (LOGN - S0)) | ulow;
+        double x[R];
+        if constexpr (SRC == 1) {
+            static_assert(UPT == 1 && R == E, "register input needs one radix-E unit per thread");
+#pragma unroll
+            for (int m = 0; m < R; ++m) x[m] = u2d(in[m]);
+        } else {
+#pragma unroll
+            for (int m = 0; m < R; ++m) x[m] = sm[pad(base + (m << LB))];
+        }
+#pragma unroll
+        for (int q = RB - 1; q >= 0; --q) {
+            const int half = R >> (q + 1);
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                if (m & half) continue;
+                const double a = x[m], b = x[m + half];
+                if (S0 + q == 0) {
+                    x[m] = fmul(a + b, last_u, p);
+                    x[m + half] = fmul(a - b, last_v, p);
+                } else {
+                    const double2 w = itw[(1 << (S0 + q)) + (uhigh << q) + (m >> (RB - q))];
+                    x[m] = a + b;
+                    x[m + half] = fmul(a - b, w, p);
+                }
+            }
+        }
+        if constexpr (DST == 1) {
+#pragma unroll
+            for (int m = 0; m < R; ++m) store(base + (m << LB), fcanon(x[m], p, pinv));
+        } else {
+            // the additive path grew by up to 2^RB: re-centre before the next group
+#pragma unroll
+            for (int m = 0; m < R; ++m) sm[pad(base + (m << LB))] = fred(x[m], p, pinv);
+        }
+    }
+}
+
+template <int LOGN, int E, int GI, class Store>
+HD void inv_main_groups_fp(double *sm, const double2 *__restrict__ itw, double p, double pinv, const u64 (&in)[E],
+                           Store &store, double2 last_u, double2 last_v) {
+    using S = Shape<LOGN, E>;
+    constexpr int S0 = S::REM + S::LOGE * GI;
+    constexpr bool first = (GI == S::G - 1);
+    constexpr bool last = (S0 == 0);
+    inv_group_fp<LOGN, E, S::LOGE, S0, first ? 1 : 0, last ? 1 : 0>(sm, itw, p, pinv, in, store, last_u, last_v);
+    if constexpr (GI > 0) {
+        __syncthreads();
+        inv_main_groups_fp<LOGN, E, GI - 1>(sm, itw, p, pinv, in, store, last_u, last_v);
+    }
+}
+
+template <int LOGN, int E = 16, class Store>
+__device__ void inverse_fp(double *sm, const double2 *__restrict__ itw, double p, double pinv, const u64 (&in)[E],
+                           Store store, double2 last_u, double2 last_v) {
+    using S = Shape<LOGN, E>;
+    static_assert(LOGN >= 6 && LOGN <= 14, "single-CTA engine covers N = 64 .. 16384");
+    __syncthreads();
+    inv_main_groups_fp<LOGN, E, S::G - 1>(sm, itw, p, pinv, in, store, last_u, last_v);
+    if constexpr (S::REM) {
+        __syncthreads();
+        inv_group_fp<LOGN, E, S::REM, 0, 0, 1>(sm, itw, p, pinv, in, store, last_u, last_v);
+    }
+}
+
 }  // namespace ntt

@@ -9,11 +9,11 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ntt_fwd
                                                                    int64_t bstride) {
     extern __shared__ u64 sm[];
     const int r = blockIdx.x, prime = row0 + r;
-    const u64 p = K.pi[prime].p;
+    const PrimeInfo P = K.pi[prime];
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         u64 *row = data + b * bstride + ((int64_t)r << LOGN);
         u64 y[16];
-        ntt::forward<LOGN>(sm, tw_row<LOGN>(K, prime), p, [&](int i) { return row[i]; }, y);
+        fwd_any<LOGN>(K, prime, P, sm, [&](int i) { return row[i]; }, y);
         __syncthreads();  // all reads of `row` done before in-place writes
         store16(row + threadIdx.x * 16, y);
     }
@@ -24,14 +24,12 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ntt_inv
                                                                    int64_t bstride) {
     extern __shared__ u64 sm[];
     const int r = blockIdx.x, prime = row0 + r;
-    const u64 p = K.pi[prime].p;
-    const LastConst lc = K.last[prime];
+    const PrimeInfo P = K.pi[prime];
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         u64 *row = data + b * bstride + ((int64_t)r << LOGN);
         u64 x[16];
         load16(row + threadIdx.x * 16, x);
-        ntt::inverse<LOGN>(sm, itw_row<LOGN>(K, prime), p, x, [&](int i, u64 v) { row[i] = v; }, lc.u_plain,
-                           lc.v_plain);
+        inv_any<LOGN>(K, prime, P, sm, x, [&](int i, u64 v) { row[i] = v; }, false);
     }
 }
 
@@ -75,7 +73,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_spread_
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         const i64 *src = coeffs + (b << LOGN);
         u64 y[16];
-        ntt::forward<LOGN>(sm, tw_row<LOGN>(K, r), P.p,
+        fwd_any<LOGN>(K, r, P, sm,
                            [&](int i) { return signed_mul_const(src[i], P.rmod, P.rmod_s, P.p); }, y);
         store16(out + b * ostride + ((int64_t)r << LOGN) + threadIdx.x * 16, y);
     }
@@ -113,13 +111,13 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_encrypt
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         auto spread = [&](const i64 *src) { return [=](int i) { return signed_mul_const(src[i], P.rmod, P.rmod_s, P.p); }; };
         u64 V[16], E[16], pk[16], o[16];
-        ntt::forward<LOGN>(sm, tw, P.p, spread(v + b * n), V);
-        ntt::forward<LOGN>(sm, tw, P.p, spread(e0m + b * n), E);
+        fwd_any<LOGN>(K, r, P, sm, spread(v + b * n), V);
+        fwd_any<LOGN>(K, r, P, sm, spread(e0m + b * n), E);
         load16(pkb + ((size_t)r << LOGN) + pos, pk);
 #pragma unroll
         for (int m = 0; m < 16; ++m) o[m] = add_mod(mont_mul(V[m], pk[m], P.p, P.pinv), E[m], P.p);
         store16(at(out, b, 0, r, LOGN) + pos, o);
-        ntt::forward<LOGN>(sm, tw, P.p, spread(e1 + b * n), E);
+        fwd_any<LOGN>(K, r, P, sm, spread(e1 + b * n), E);
         load16(pka + ((size_t)r << LOGN) + pos, pk);
 #pragma unroll
         for (int m = 0; m < 16; ++m) o[m] = add_mod(mont_mul(V[m], pk[m], P.p, P.pinv), E[m], P.p);
@@ -162,7 +160,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_decrypt
 #pragma unroll
         for (int m = 0; m < 16; ++m) x[m] = add_mod(mont_mul(x[m], y[m], P.p, P.pinv), z[m], P.p);
         u64 *dst = tmp + (b * rows + r) * n;
-        ntt::inverse<LOGN>(sm, itw_row<LOGN>(K, r), P.p, x, [&](int i, u64 v) { dst[i] = v; }, lc.u_std, lc.v_std);
+        inv_any<LOGN>(K, r, P, sm, x, [&](int i, u64 v) { dst[i] = v; }, true);
     }
 }
 
@@ -221,7 +219,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_make_pk
     const PrimeInfo P = K.pi[r];
     const int pos = threadIdx.x * 16;
     u64 E[16], x[16], y[16];
-    ntt::forward<LOGN>(sm, tw_row<LOGN>(K, r), P.p,
+    fwd_any<LOGN>(K, r, P, sm,
                        [&](int i) { return signed_mul_const(e[i], P.rmod, P.rmod_s, P.p); }, E);
     const size_t off = ((size_t)r << LOGN) + pos;
     load16(a + off, x);
@@ -242,7 +240,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_make_sw
     const int pos = threadIdx.x * 16;
     const i64 *ej = e + ((size_t)j << LOGN);
     u64 E[16], x[16], y[16];
-    ntt::forward<LOGN>(sm, tw_row<LOGN>(K, r), P.p,
+    fwd_any<LOGN>(K, r, P, sm,
                        [&](int i) { return signed_mul_const(ej[i], P.rmod, P.rmod_s, P.p); }, E);
     const size_t off = (((size_t)j * R + r) << LOGN) + pos;
     load16(a + off, x);
