@@ -63,7 +63,7 @@ struct LevelConst {
 struct LastConst {  // final inverse-stage factors (Shoup pairs; FP64 engine: (w, w/p))
     ulonglong2 u_plain, v_plain;  // n^-1,       itw[1] n^-1
     ulonglong2 u_std, v_std;      // n^-1 R^-1,  itw[1] n^-1 R^-1  (fold from-Montgomery)
-    double2 fu_plain, fv_plain, fu_std, fv_std;
+    double fu_plain, fv_plain, fu_std, fv_std;
 };
 
 struct heb_ctx {
@@ -71,7 +71,7 @@ struct heb_ctx {
     std::vector<u64> primes;
     PrimeInfo *d_pi = nullptr;
     ulonglong2 *d_tw = nullptr, *d_itw = nullptr;
-    double2 *d_twf = nullptr, *d_itwf = nullptr;  // FP64 engine tables (w, w/p)
+    double *d_twf = nullptr, *d_itwf = nullptr;  // FP64 engine twiddles (w as double)
     LevelConst *d_lc = nullptr;
     LastConst *d_last = nullptr;
     int flush = 64;  // lazy 128-bit accumulation: products summed before a reduction
@@ -94,7 +94,7 @@ struct Scratch {
 struct Ctx {  // kernel-side view of the context
     const PrimeInfo *pi;
     const ulonglong2 *tw, *itw;
-    const double2 *twf, *itwf;
+    const double *twf, *itwf;
     const LevelConst *lc;
     const LastConst *last;
     int num_rows;
@@ -142,7 +142,7 @@ __device__ __forceinline__ void load16(const u64 *__restrict__ src, u64 (&v)[16]
     const ulonglong2 *s = reinterpret_cast<const ulonglong2 *>(src);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        ulonglong2 t = s[i];
+        ulonglong2 t = __ldcg(s + i);
         v[2 * i] = t.x;
         v[2 * i + 1] = t.y;
     }
@@ -150,7 +150,7 @@ __device__ __forceinline__ void load16(const u64 *__restrict__ src, u64 (&v)[16]
 __device__ __forceinline__ void store16(u64 *__restrict__ dst, const u64 (&v)[16]) {
     ulonglong2 *d = reinterpret_cast<ulonglong2 *>(dst);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) d[i] = make_ulonglong2(v[2 * i], v[2 * i + 1]);
+    for (int i = 0; i < 8; ++i) __stcg(d + i, make_ulonglong2(v[2 * i], v[2 * i + 1]));
 }
 
 // minimum resident CTAs per SM for the NTT kernels: caps registers at 64/thread

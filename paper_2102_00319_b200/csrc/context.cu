@@ -89,7 +89,7 @@ extern "C" int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows
     }
     std::vector<PrimeInfo> pi(num_rows);
     std::vector<ulonglong2> tw((size_t)num_rows * n), itw((size_t)num_rows * n);
-    std::vector<double2> twf((size_t)num_rows * n), itwf((size_t)num_rows * n);
+    std::vector<double> twf((size_t)num_rows * n), itwf((size_t)num_rows * n);
     std::vector<LastConst> last(num_rows);
     const char *fp_env = getenv("HEB_DISABLE_FP64_NTT");
     const bool fp_disabled = fp_env && fp_env[0] == '1';
@@ -131,7 +131,7 @@ extern "C" int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows
         q.pd = (double)p;
         q.pinvd = 1.0 / (double)p;
         q.use_fp = (p < (1ull << 42)) && !fp_disabled;
-        auto fpair = [&](u64 w) { return make_double2((double)w, (double)w / (double)p); };
+        auto fpair = [&](u64 w) { return (double)w; };
         for (int i = 0; i < n; ++i) {
             twf[(size_t)r * n + i] = fpair(tw[(size_t)r * n + i].x);
             itwf[(size_t)r * n + i] = fpair(itw[(size_t)r * n + i].x);
@@ -172,10 +172,10 @@ extern "C" int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows
         (e = cudaMalloc(&c->d_pi, sizeof(PrimeInfo) * num_rows)) != cudaSuccess ||
         (e = cudaMalloc(&c->d_tw, sizeof(ulonglong2) * tw.size())) != cudaSuccess ||
         (e = cudaMalloc(&c->d_itw, sizeof(ulonglong2) * itw.size())) != cudaSuccess ||
-        (e = cudaMalloc(&c->d_twf, sizeof(double2) * twf.size())) != cudaSuccess ||
-        (e = cudaMalloc(&c->d_itwf, sizeof(double2) * itwf.size())) != cudaSuccess ||
-        (e = cudaMemcpy(c->d_twf, twf.data(), sizeof(double2) * twf.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
-        (e = cudaMemcpy(c->d_itwf, itwf.data(), sizeof(double2) * itwf.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMalloc(&c->d_twf, sizeof(double) * twf.size())) != cudaSuccess ||
+        (e = cudaMalloc(&c->d_itwf, sizeof(double) * itwf.size())) != cudaSuccess ||
+        (e = cudaMemcpy(c->d_twf, twf.data(), sizeof(double) * twf.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(c->d_itwf, itwf.data(), sizeof(double) * itwf.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
         (e = cudaMalloc(&c->d_lc, sizeof(LevelConst) * lc.size())) != cudaSuccess ||
         (e = cudaMalloc(&c->d_last, sizeof(LastConst) * num_rows)) != cudaSuccess ||
         (e = cudaMemcpy(c->d_pi, pi.data(), sizeof(PrimeInfo) * num_rows, cudaMemcpyHostToDevice)) != cudaSuccess ||

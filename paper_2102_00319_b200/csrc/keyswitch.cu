@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_rescale
         const i64 *src = V + (b * comps + c) * (1 << LOGN);
         u64 y[16];
         fwd_any<LOGN>(K, i, P, sm,
-                           [&](int j) { return signed_mul_const(src[j], C.beta_r.x, C.beta_r.y, P.p); }, y);
+                           [&](int j) { return signed_mul_const(__ldcg(src + j), C.beta_r.x, C.beta_r.y, P.p); }, y);
         u64 x[16];
         load16(at(in, b, c, i, LOGN) + threadIdx.x * 16, x);
         if (pt) {
@@ -122,54 +122,62 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_head
 // ulonglong2 pairs (w, floor(w 2^64 / p)) of the b part (N entries) then the a part,
 // with w the key residue in standard form, so dig * key is one Shoup product that
 // keeps dig's Montgomery factor (identical to the reference's mont_mul(dig, evk)).
-// The accumulators stay in registers across the digit loop, so this kernel uses the
-// E = 8 engine variant (N/8 threads, 8 positions per thread) to keep the per-thread
-// working set small enough for full occupancy without spills.
-#define MODUP_E(LOGN) ((LOGN) >= 14 ? 16 : 8)
-#define MODUP_MINB(LOGN) ((1024 / ntt::Shape<LOGN, MODUP_E(LOGN)>::T) > 32 ? 32 : (1024 / ntt::Shape<LOGN, MODUP_E(LOGN)>::T))
-
+//
+// ModUp is split in two launches so that the transform kernel carries no
+// accumulators (full register budget, two CTAs per SM, independent phases):
+//   k_ks_modup_ntt : one CTA per (item, digit j, target t != j):
+//                    V[item][t][j] = NTT_t(D_j mod p_t * R)        (k^2 NTTs/item)
+//   k_ks_modup_mac : pointwise, acc_t = sum_j v_j (*) key[j][t] with v_t = d2_t
+//                    (the centred digit is congruent to d2_t mod its own prime).
+// V layout: (count, k+1, k, N); slot (t, t) is unused.
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN, MODUP_E(LOGN)>::T, MODUP_MINB(LOGN))
-    k_ks_modup(Ctx K, heb_ct src, int comp, const i64 *D, const ulonglong2 *key, int k, u64 *acc, int64_t count) {
-    constexpr int E = MODUP_E(LOGN);
+__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN))
+    k_ks_modup_ntt(Ctx K, const i64 *D, int k, u64 *V, int64_t count) {
     extern __shared__ u64 sm[];
-    const int t = blockIdx.x;
+    // blockIdx.x enumerates the k^2 (t, j) pairs with j != t: k-1 digits for each
+    // ciphertext target t < k, then all k digits for the special prime (t = k)
+    const int x = blockIdx.x;
+    int t, j;
+    if (x < k * (k - 1)) {
+        t = x / (k - 1);
+        j = x % (k - 1);
+        j += (j >= t);
+    } else {
+        t = k;
+        j = x - k * (k - 1);
+    }
+    const int gt = t < k ? t : K.num_rows - 1;
+    const PrimeInfo P = K.pi[gt];
+    const int n = 1 << LOGN;
+    for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
+        const i64 *dj = D + (b * k + j) * n;
+        u64 y[16];
+        fwd_any<LOGN>(K, gt, P, sm, [&](int i) { return signed_mul_const(__ldcg(dj + i), P.rmod, P.rmod_s, P.p); }, y);
+        store16(V + ((b * (k + 1) + t) * k + j) * n + threadIdx.x * 16, y);
+    }
+}
+
+// acc[item][c][t][x] = sum_j v_j[x] * key_c[j][gt][x]  (Shoup with the prepared key)
+__global__ void k_ks_modup_mac(Ctx K, heb_ct src, int comp, const u64 *V, const ulonglong2 *key, int k, u64 *acc,
+                               int64_t count, int logn) {
+    const int n = 1 << logn;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.y;
     const int gt = t < k ? t : K.num_rows - 1;
     const PrimeInfo P = K.pi[gt];
     const u64 p2 = 2 * P.p;
-    const int n = 1 << LOGN;
-    const int pos = threadIdx.x * E;
-    for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
-        u64 a0[E], a1[E];
-#pragma unroll
-        for (int m = 0; m < E; ++m) a0[m] = a1[m] = 0;
+    if (x >= n) return;
+    for (int64_t b = blockIdx.z; b < count; b += gridDim.z) {
+        u64 s0 = 0, s1 = 0;
         for (int j = 0; j < k; ++j) {
-            u64 dig[E];
-            if (j == t) {
-                const u64 *s = at(src, b, comp, j, LOGN) + pos;
-#pragma unroll
-                for (int m = 0; m < E; ++m) dig[m] = s[m];
-            } else {
-                const i64 *dj = D + (b * k + j) * n;
-                fwd_any<LOGN, E>(K, gt, P, sm,
-                                      [&](int i) { return signed_mul_const(dj[i], P.rmod, P.rmod_s, P.p); }, dig);
-            }
-            const ulonglong2 *kb = key + (((size_t)j * K.num_rows + gt) * 2) * n + pos;
-            const ulonglong2 *ka = kb + n;
-#pragma unroll
-            for (int m = 0; m < E; ++m) {
-                const ulonglong2 wb = kb[m], wa = ka[m];
-                a0[m] = csub(a0[m] + shoup_lazy(dig[m], wb.x, wb.y, P.p), p2);
-                a1[m] = csub(a1[m] + shoup_lazy(dig[m], wa.x, wa.y, P.p), p2);
-            }
+            const u64 v = (j == t) ? __ldcg(at(src, b, comp, j, logn) + x) : __ldcg(V + ((b * (k + 1) + t) * k + j) * n + x);
+            const ulonglong2 *kb = key + (((size_t)j * K.num_rows + gt) * 2) * n + x;
+            const ulonglong2 wb = __ldg(kb), wa = __ldg(kb + n);
+            s0 = csub(s0 + shoup_lazy(v, wb.x, wb.y, P.p), p2);
+            s1 = csub(s1 + shoup_lazy(v, wa.x, wa.y, P.p), p2);
         }
-        u64 *o0 = acc + ((b * 2 + 0) * (k + 1) + t) * n + pos;
-        u64 *o1 = acc + ((b * 2 + 1) * (k + 1) + t) * n + pos;
-#pragma unroll
-        for (int m = 0; m < E; ++m) {
-            o0[m] = csub(a0[m], P.p);
-            o1[m] = csub(a1[m], P.p);
-        }
+        __stcg(acc + ((b * 2 + 0) * (k + 1) + t) * n + x, csub(s0, P.p));
+        __stcg(acc + ((b * 2 + 1) * (k + 1) + t) * n + x, csub(s1, P.p));
     }
 }
 
@@ -257,9 +265,9 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_down
         u64 y[16];
         fwd_any<LOGN>(K, i, Pi, sm,
             [&](int j) {
-                const i64 a = ap[j];
+                const i64 a = __ldcg(ap + j);
                 // s_L = (bL - aP) * P^-1 mod q_L, centred
-                const u64 sl = sub_mod(shoup(bl[j], CL.pinv.x, CL.pinv.y, PL.p),
+                const u64 sl = sub_mod(shoup(__ldcg(bl + j), CL.pinv.x, CL.pinv.y, PL.p),
                                        signed_mul_const(a, CL.pinv.x, CL.pinv.y, PL.p), PL.p);
                 const i64 cl = center(sl, PL.p);
                 return add_mod(signed_mul_const(a, Ci.alpha_r.x, Ci.alpha_r.y, Pi.p),
@@ -292,7 +300,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_down
         const i64 *ap = aP + (b * 2 + c) * n;
         u64 y[16];
         fwd_any<LOGN>(K, i, Pi, sm,
-                           [&](int j) { return signed_mul_const(ap[j], Ci.gamma_r.x, Ci.gamma_r.y, Pi.p); }, y);
+                           [&](int j) { return signed_mul_const(__ldcg(ap + j), Ci.gamma_r.x, Ci.gamma_r.y, Pi.p); }, y);
         u64 x[16];
         load16(acc + ((b * 2 + c) * (k + 1) + i) * n + pos, x);
 #pragma unroll
@@ -313,18 +321,21 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
     constexpr int T = ntt::Shape<LOGN>::T;
     constexpr size_t sm = smem_bytes<LOGN>();
     CUDA_TRY(prep_kernel(k_ks_head<LOGN>, sm));
-    CUDA_TRY(prep_kernel(k_ks_modup<LOGN>, sm));
+    CUDA_TRY(prep_kernel(k_ks_modup_ntt<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_ks_down_head<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_ks_down_rescale_tail<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_ks_down_tail<LOGN>, sm));
     const int k = level + 1, n = c->n;
     const int64_t chunk = c->chunk > 0 ? c->chunk : count;
     const int64_t cmax = std::min<int64_t>(chunk, count);
-    Scratch sD(st), sA(st), sP(st), sL(st);
+    // ModUp sub-chunk: enough (item, t, j) transforms for ~8 CTA waves, V kept small
+    const int64_t sub = std::max<int64_t>(8, std::min<int64_t>(cmax, (2400 + k * k - 1) / (k * k)));
+    Scratch sD(st), sA(st), sP(st), sL(st), sV(st);
     CUDA_TRY(sD.get(sizeof(i64) * (size_t)cmax * k * n));
     CUDA_TRY(sA.get(sizeof(u64) * (size_t)cmax * 2 * (k + 1) * n));
     CUDA_TRY(sP.get(sizeof(i64) * (size_t)cmax * 2 * n));
     CUDA_TRY(sL.get(sizeof(u64) * (size_t)cmax * 2 * n));
+    CUDA_TRY(sV.get(sizeof(u64) * (size_t)sub * (k + 1) * k * n));
     const Ctx K = kctx(c);
     for (int64_t b0 = 0; b0 < count; b0 += chunk) {
         const int64_t cnt = std::min<int64_t>(chunk, count - b0);
@@ -335,8 +346,24 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
         const unsigned gy = gdim(cnt);
         { PROF("k_ks_head", st, 16.0 * n * cnt * k); k_ks_head<LOGN><<<dim3(k, gy), T, sm, st>>>(K, s, comp, (i64 *)sD.p, k, cnt); }
         LAUNCH_CHECK();
-        { PROF("k_ks_modup", st, 8.0 * n * (2.0 * cnt * k + 2.0 * k * (k + 1) + 2.0 * cnt * (k + 1))); k_ks_modup<LOGN><<<dim3(k + 1, gy), ntt::Shape<LOGN, MODUP_E(LOGN)>::T, sm, st>>>(K, s, comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt); }
-        LAUNCH_CHECK();
+        for (int64_t s0 = 0; s0 < cnt; s0 += sub) {
+            const int64_t sc = std::min<int64_t>(sub, cnt - s0);
+            heb_ct ss = s;
+            ss.data += s0 * s.ct_stride;
+            const i64 *Dp = (const i64 *)sD.p + s0 * k * n;
+            u64 *Ap = (u64 *)sA.p + s0 * 2 * (k + 1) * n;
+            {
+                PROF("k_ks_modup_ntt", st, 16.0 * n * sc * k * k);
+                k_ks_modup_ntt<LOGN><<<dim3(k * k, gdim(sc)), T, sm, st>>>(K, Dp, k, (u64 *)sV.p, sc);
+            }
+            LAUNCH_CHECK();
+            {
+                PROF("k_ks_modup_mac", st, 8.0 * n * (sc * k * (k + 1) + 4.0 * k * (k + 1) + 2.0 * sc * (k + 1)));
+                k_ks_modup_mac<<<dim3((n + 255) / 256, k + 1, gdim(sc)), 256, 0, st>>>(K, ss, comp, (const u64 *)sV.p,
+                                                                                        key, k, Ap, sc, LOGN);
+            }
+            LAUNCH_CHECK();
+        }
         if (rescale) {
             { PROF("k_ks_down_head", st, 8.0 * n * cnt * 10.0); k_ks_down_head<LOGN><<<dim3(2, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
                                                                  (u64 *)sL.p, cnt); }

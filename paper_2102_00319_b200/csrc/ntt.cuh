@@ -71,7 +71,7 @@ HD void fwd_group(u64 *sm, const ulonglong2 *__restrict__ tw, u64 p, Load &load,
 #pragma unroll
             for (int m = 0; m < R; ++m) {
                 if (m & half) continue;
-                const ulonglong2 w = tw[(1 << (S0 + q)) + (uhigh << q) + (m >> (RB - q))];
+                const ulonglong2 w = __ldg(tw + (1 << (S0 + q)) + (uhigh << q) + (m >> (RB - q)));
                 u64 a = csub(x[m], p2);
                 u64 t = shoup_lazy(x[m + half], w.x, w.y, p);
                 x[m] = a + t;
@@ -154,7 +154,7 @@ HD void inv_group(u64 *sm, const ulonglong2 *__restrict__ itw, u64 p, const u64 
                     x[m] = shoup(a + b, last_u.x, last_u.y, p);
                     x[m + half] = shoup(a - b + p2, last_v.x, last_v.y, p);
                 } else {
-                    const ulonglong2 w = itw[(1 << (S0 + q)) + (uhigh << q) + (m >> (RB - q))];
+                    const ulonglong2 w = __ldg(itw + (1 << (S0 + q)) + (uhigh << q) + (m >> (RB - q)));
                     x[m] = csub(a + b, p2);
                     x[m + half] = shoup_lazy(a - b + p2, w.x, w.y, p);
                 }
@@ -219,11 +219,12 @@ __device__ void inverse(u64 *sm, const ulonglong2 *__restrict__ itw, u64 p, cons
 
 HD double u2d(u64 v) { return __longlong_as_double((long long)(0x4330000000000000ull | v)) - 4503599627370496.0; }
 HD double rint_fp(double x) { return (x + FP_MAGIC) - FP_MAGIC; }
-// y * w mod p, result in (-p, 2p); w2 = (w, w/p)
-HD double fmul(double y, double2 w2, double p) {
-    const double h = __dmul_rn(y, w2.x);
-    const double l = fma(y, w2.x, -h);
-    const double q = __dsub_rn(fma(y, w2.y, FP_MAGIC), FP_MAGIC);
+// y * w mod p, result in (-p, 2p); the quotient estimate uses the rounded product
+// h (relative error 2^-52), so it is off by at most one -- absorbed by the lazy range
+HD double fmul(double y, double w, double p, double pinv) {
+    const double h = __dmul_rn(y, w);
+    const double l = fma(y, w, -h);
+    const double q = __dsub_rn(fma(h, pinv, FP_MAGIC), FP_MAGIC);
     return __dadd_rn(fma(-q, p, h), l);
 }
 // any |x| < 2^50 -> centred representative in about (-p/2, p/2]
@@ -240,7 +241,7 @@ HD u64 fcanon(double x, double p, double pinv) {
 }
 
 template <int LOGN, int E, int RB, int S0, int SRC, int DST, class Load>
-HD void fwd_group_fp(double *sm, const double2 *__restrict__ tw, double p, double pinv, Load &load,
+HD void fwd_group_fp(double *sm, const double *__restrict__ tw, double p, double pinv, Load &load,
                      u64 (&out)[E]) {
     using S = Shape<LOGN, E>;
     constexpr int R = 1 << RB;
@@ -266,8 +267,8 @@ HD void fwd_group_fp(double *sm, const double2 *__restrict__ tw, double p, doubl
 #pragma unroll
             for (int m = 0; m < R; ++m) {
                 if (m & half) continue;
-                const double2 w = tw[(1 << (S0 + q)) + (uhigh << q) + (m >> (RB - q))];
-                const double r = fmul(x[m + half], w, p);
+                const double w = __ldg(tw + (1 << (S0 + q)) + (uhigh << q) + (m >> (RB - q)));
+                const double r = fmul(x[m + half], w, p, pinv);
                 x[m + half] = x[m] - r;
                 x[m] = x[m] + r;
             }
@@ -284,7 +285,7 @@ HD void fwd_group_fp(double *sm, const double2 *__restrict__ tw, double p, doubl
 }
 
 template <int LOGN, int E, int GI, class Load>
-HD void fwd_main_groups_fp(double *sm, const double2 *__restrict__ tw, double p, double pinv, Load &load,
+HD void fwd_main_groups_fp(double *sm, const double *__restrict__ tw, double p, double pinv, Load &load,
                            u64 (&out)[E]) {
     using S = Shape<LOGN, E>;
     constexpr int S0 = S::REM + S::LOGE * GI;
@@ -298,7 +299,7 @@ HD void fwd_main_groups_fp(double *sm, const double2 *__restrict__ tw, double p,
 }
 
 template <int LOGN, int E = 16, class Load>
-__device__ void forward_fp(double *sm, const double2 *__restrict__ tw, double p, double pinv, Load load,
+__device__ void forward_fp(double *sm, const double *__restrict__ tw, double p, double pinv, Load load,
                            u64 (&out)[E]) {
     using S = Shape<LOGN, E>;
     static_assert(LOGN >= 6 && LOGN <= 14, "single-CTA engine covers N = 64 .. 16384");
@@ -311,8 +312,8 @@ __device__ void forward_fp(double *sm, const double2 *__restrict__ tw, double p,
 }
 
 template <int LOGN, int E, int RB, int S0, int SRC, int DST, class Store>
-HD void inv_group_fp(double *sm, const double2 *__restrict__ itw, double p, double pinv, const u64 (&in)[E],
-                     Store &store, double2 last_u, double2 last_v) {
+HD void inv_group_fp(double *sm, const double *__restrict__ itw, double p, double pinv, const u64 (&in)[E],
+                     Store &store, double last_u, double last_v) {
     using S = Shape<LOGN, E>;
     constexpr int R = 1 << RB;
     constexpr int LB = LOGN - S0 - RB;
@@ -341,12 +342,12 @@ HD void inv_group_fp(double *sm, const double2 *__restrict__ itw, double p, doub
                 if (m & half) continue;
                 const double a = x[m], b = x[m + half];
                 if (S0 + q == 0) {
-                    x[m] = fmul(a + b, last_u, p);
-                    x[m + half] = fmul(a - b, last_v, p);
+                    x[m] = fmul(a + b, last_u, p, pinv);
+                    x[m + half] = fmul(a - b, last_v, p, pinv);
                 } else {
-                    const double2 w = itw[(1 << (S0 + q)) + (uhigh << q) + (m >> (RB - q))];
+                    const double w = __ldg(itw + (1 << (S0 + q)) + (uhigh << q) + (m >> (RB - q)));
                     x[m] = a + b;
-                    x[m + half] = fmul(a - b, w, p);
+                    x[m + half] = fmul(a - b, w, p, pinv);
                 }
             }
         }
@@ -362,8 +363,8 @@ HD void inv_group_fp(double *sm, const double2 *__restrict__ itw, double p, doub
 }
 
 template <int LOGN, int E, int GI, class Store>
-HD void inv_main_groups_fp(double *sm, const double2 *__restrict__ itw, double p, double pinv, const u64 (&in)[E],
-                           Store &store, double2 last_u, double2 last_v) {
+HD void inv_main_groups_fp(double *sm, const double *__restrict__ itw, double p, double pinv, const u64 (&in)[E],
+                           Store &store, double last_u, double last_v) {
     using S = Shape<LOGN, E>;
     constexpr int S0 = S::REM + S::LOGE * GI;
     constexpr bool first = (GI == S::G - 1);
@@ -376,8 +377,8 @@ HD void inv_main_groups_fp(double *sm, const double2 *__restrict__ itw, double p
 }
 
 template <int LOGN, int E = 16, class Store>
-__device__ void inverse_fp(double *sm, const double2 *__restrict__ itw, double p, double pinv, const u64 (&in)[E],
-                           Store store, double2 last_u, double2 last_v) {
+__device__ void inverse_fp(double *sm, const double *__restrict__ itw, double p, double pinv, const u64 (&in)[E],
+                           Store store, double last_u, double last_v) {
     using S = Shape<LOGN, E>;
     static_assert(LOGN >= 6 && LOGN <= 14, "single-CTA engine covers N = 64 .. 16384");
     __syncthreads();

@@ -13,7 +13,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ntt_fwd
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         u64 *row = data + b * bstride + ((int64_t)r << LOGN);
         u64 y[16];
-        fwd_any<LOGN>(K, prime, P, sm, [&](int i) { return row[i]; }, y);
+        fwd_any<LOGN>(K, prime, P, sm, [&](int i) { return __ldcg(row + i); }, y);
         __syncthreads();  // all reads of `row` done before in-place writes
         store16(row + threadIdx.x * 16, y);
     }
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_spread_
         const i64 *src = coeffs + (b << LOGN);
         u64 y[16];
         fwd_any<LOGN>(K, r, P, sm,
-                           [&](int i) { return signed_mul_const(src[i], P.rmod, P.rmod_s, P.p); }, y);
+                           [&](int i) { return signed_mul_const(__ldcg(src + i), P.rmod, P.rmod_s, P.p); }, y);
         store16(out + b * ostride + ((int64_t)r << LOGN) + threadIdx.x * 16, y);
     }
 }
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_encrypt
     const int n = 1 << LOGN, pos = threadIdx.x * 16;
     const ulonglong2 *tw = tw_row<LOGN>(K, r);
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
-        auto spread = [&](const i64 *src) { return [=](int i) { return signed_mul_const(src[i], P.rmod, P.rmod_s, P.p); }; };
+        auto spread = [&](const i64 *src) { return [=](int i) { return signed_mul_const(__ldcg(src + i), P.rmod, P.rmod_s, P.p); }; };
         u64 V[16], E[16], pk[16], o[16];
         fwd_any<LOGN>(K, r, P, sm, spread(v + b * n), V);
         fwd_any<LOGN>(K, r, P, sm, spread(e0m + b * n), E);
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_make_pk
     const int pos = threadIdx.x * 16;
     u64 E[16], x[16], y[16];
     fwd_any<LOGN>(K, r, P, sm,
-                       [&](int i) { return signed_mul_const(e[i], P.rmod, P.rmod_s, P.p); }, E);
+                       [&](int i) { return signed_mul_const(__ldcg(e + i), P.rmod, P.rmod_s, P.p); }, E);
     const size_t off = ((size_t)r << LOGN) + pos;
     load16(a + off, x);
     load16(s + off, y);
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_make_sw
     const i64 *ej = e + ((size_t)j << LOGN);
     u64 E[16], x[16], y[16];
     fwd_any<LOGN>(K, r, P, sm,
-                       [&](int i) { return signed_mul_const(ej[i], P.rmod, P.rmod_s, P.p); }, E);
+                       [&](int i) { return signed_mul_const(__ldcg(ej + i), P.rmod, P.rmod_s, P.p); }, E);
     const size_t off = (((size_t)j * R + r) << LOGN) + pos;
     load16(a + off, x);
     load16(s + ((size_t)r << LOGN) + pos, y);
