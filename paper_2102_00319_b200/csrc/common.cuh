@@ -103,29 +103,96 @@ static inline Ctx kctx(const heb_ctx *c) {
     return Ctx{c->d_pi, c->d_tw, c->d_itw, c->d_twf, c->d_itwf, c->d_lc, c->d_last, c->num_rows};
 }
 
+// ---------------------------------------------------------------------------------
+// Row geometry.  Rows of N <= 2^14 residues are owned by one CTA; N = 2^15 rows are
+// split over a 2-CTA cluster (blockIdx.x = 2 * logical index + half).  Kernels use
+// lbx() for their logical x index, tpos() for the first of the E positions a thread
+// holds after a forward transform, KT for their block size.
+template <int LOGN>
+struct Row {
+    static constexpr bool SPLIT = LOGN > 14;
+    static constexpr int LL = SPLIT ? LOGN - 1 : LOGN;  // residues per CTA = 2^LL
+    static constexpr int N = 1 << LOGN;
+};
+template <int LOGN, int E = 16>
+constexpr int KT = ntt::Shape<Row<LOGN>::LL, E>::T;
+template <int LOGN>
+__device__ __forceinline__ int lbx() {
+    return Row<LOGN>::SPLIT ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+}
+template <int LOGN>
+__device__ __forceinline__ int rhalf() {
+    return Row<LOGN>::SPLIT ? (int)(blockIdx.x & 1) : 0;
+}
+template <int LOGN, int E = 16>
+__device__ __forceinline__ int tpos() {
+    return (rhalf<LOGN>() << Row<LOGN>::LL) + (int)threadIdx.x * E;
+}
+
 // Row-dispatched transforms: rows whose prime is < 2^42 run on the FP64 engine, the
 // others (50/60-bit base and special primes) on the 64-bit integer engine.  Both read
 // u64 residues and return canonical u64 residues, so callers are engine-agnostic.
 template <int LOGN, int E = 16, class Load>
 __device__ __forceinline__ void fwd_any(const Ctx &K, int row, const PrimeInfo &P, u64 *sm, Load load,
                                         u64 (&out)[E]) {
-    if (P.use_fp)
-        ntt::forward_fp<LOGN, E>(reinterpret_cast<double *>(sm), K.twf + ((size_t)row << LOGN), P.pd, P.pinvd, load,
-                                 out);
-    else
-        ntt::forward<LOGN, E>(sm, K.tw + ((size_t)row << LOGN), P.p, load, out);
+    constexpr int LL = Row<LOGN>::LL;
+    if (P.use_fp) {
+        const ntt::FpArith ar(P.pd, P.pinvd);
+        double *s = reinterpret_cast<double *>(sm);
+        const double *tw = K.twf + ((size_t)row << LOGN);
+        if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, E>(ar, s, tw, load, out, rhalf<LOGN>());
+        else ntt::forward<LL, E>(ar, s, tw, load, out);
+    } else {
+        const ntt::IntArith ar(P.p);
+        const ulonglong2 *tw = K.tw + ((size_t)row << LOGN);
+        if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, E>(ar, sm, tw, load, out, rhalf<LOGN>());
+        else ntt::forward<LL, E>(ar, sm, tw, load, out);
+    }
 }
 // std_out: fold the from-Montgomery factor R^-1 into the final stage
 template <int LOGN, int E = 16, class Store>
 __device__ __forceinline__ void inv_any(const Ctx &K, int row, const PrimeInfo &P, u64 *sm, const u64 (&in)[E],
                                         Store store, bool std_out) {
+    constexpr int LL = Row<LOGN>::LL;
     const LastConst &lc = K.last[row];
-    if (P.use_fp)
-        ntt::inverse_fp<LOGN, E>(reinterpret_cast<double *>(sm), K.itwf + ((size_t)row << LOGN), P.pd, P.pinvd, in,
-                                 store, std_out ? lc.fu_std : lc.fu_plain, std_out ? lc.fv_std : lc.fv_plain);
-    else
-        ntt::inverse<LOGN, E>(sm, K.itw + ((size_t)row << LOGN), P.p, in, store, std_out ? lc.u_std : lc.u_plain,
-                              std_out ? lc.v_std : lc.v_plain);
+    if (P.use_fp) {
+        const ntt::FpArith ar(P.pd, P.pinvd);
+        double *s = reinterpret_cast<double *>(sm);
+        const double *itw = K.itwf + ((size_t)row << LOGN);
+        const double u = std_out ? lc.fu_std : lc.fu_plain, v = std_out ? lc.fv_std : lc.fv_plain;
+        if constexpr (Row<LOGN>::SPLIT) ntt::inverse_split<LL, E>(ar, s, itw, in, store, u, v, rhalf<LOGN>());
+        else ntt::inverse<LL, E>(ar, s, itw, in, store, u, v);
+    } else {
+        const ntt::IntArith ar(P.p);
+        const ulonglong2 *itw = K.itw + ((size_t)row << LOGN);
+        const ulonglong2 u = std_out ? lc.u_std : lc.u_plain, v = std_out ? lc.v_std : lc.v_plain;
+        if constexpr (Row<LOGN>::SPLIT) ntt::inverse_split<LL, E>(ar, sm, itw, in, store, u, v, rhalf<LOGN>());
+        else ntt::inverse<LL, E>(ar, sm, itw, in, store, u, v);
+    }
+}
+
+// Launch a row kernel: split rows get twice the CTAs along x, clustered in pairs.
+template <int LOGN, class Kern, class... Args>
+static cudaError_t launch_rows(Kern kernel, dim3 grid, int block, size_t smem, cudaStream_t st, Args... args) {
+    if constexpr (Row<LOGN>::SPLIT) {
+        grid.x *= 2;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(block);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kernel, args...);
+    } else {
+        kernel<<<grid, block, smem, st>>>(args...);
+        return cudaGetLastError();
+    }
 }
 
 template <int LOGN>
@@ -157,12 +224,15 @@ __device__ __forceinline__ void store16(u64 *__restrict__ dst, const u64 (&v)[16
 #ifndef NTT_REGS_PER_THREAD
 #define NTT_REGS_PER_THREAD 64
 #endif
-#define NTT_MINB(LOGN) \
-    (((65536 / NTT_REGS_PER_THREAD) >> ((LOGN) - 4)) > 32 ? 32 : (((65536 / NTT_REGS_PER_THREAD) >> ((LOGN) - 4)) < 1 ? 1 : ((65536 / NTT_REGS_PER_THREAD) >> ((LOGN) - 4))))
+#define NTT_MINB_LL(LL) \
+    (((65536 / NTT_REGS_PER_THREAD) >> ((LL) - 4)) > 32 ? 32 : (((65536 / NTT_REGS_PER_THREAD) >> ((LL) - 4)) < 1 ? 1 : ((65536 / NTT_REGS_PER_THREAD) >> ((LL) - 4))))
+#define NTT_MINB(LOGN) NTT_MINB_LL(Row<LOGN>::LL)
+// launch bounds of a row kernel (E = 16 engine)
+#define ROW_BOUNDS(LOGN) __launch_bounds__(KT<LOGN>, NTT_MINB(LOGN))
 
 template <int LOGN>
 static constexpr size_t smem_bytes() {
-    return sizeof(u64) * ntt::Shape<LOGN>::SMEM_WORDS;
+    return sizeof(u64) * ntt::Shape<Row<LOGN>::LL>::SMEM_WORDS;
 }
 
 template <class K>
@@ -183,6 +253,7 @@ static cudaError_t prep_kernel(K kernel, size_t smem) {
         case 12: return FN<12>(__VA_ARGS__);                                 \
         case 13: return FN<13>(__VA_ARGS__);                                 \
         case 14: return FN<14>(__VA_ARGS__);                                 \
+        case 15: return FN<15>(__VA_ARGS__);                                 \
         default: return fail(HEB_EUNSUP, "unsupported log_n %d", (ctx)->log_n); \
     }
 

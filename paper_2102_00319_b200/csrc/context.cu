@@ -66,7 +66,7 @@ extern "C" int heb_device_count(int *count) {
 extern "C" int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows, const uint64_t *primes,
                               const uint64_t *psi) {
     if (!out || !primes || num_rows < 2) return fail(HEB_EINVAL, "heb_ctx_create: bad arguments");
-    if (log_n < 6 || log_n > 14) return fail(HEB_EUNSUP, "ring degree 2^%d not supported (2^6 .. 2^14)", log_n);
+    if (log_n < 6 || log_n > 15) return fail(HEB_EUNSUP, "ring degree 2^%d not supported (2^6 .. 2^15)", log_n);
     const int n = 1 << log_n;
     auto *c = new heb_ctx();
     c->device = device;

@@ -7,19 +7,19 @@
 //   tail: out_i = c_i [* pt_i] * qL^-1 - NTT_i(v * qL^-1 * R)  (k-1 NTTs / component)
 // =============================================================================
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_rescale_head(Ctx K, heb_ct in, const u64 *pt,
+__global__ void ROW_BOUNDS(LOGN) k_rescale_head(Ctx K, heb_ct in, const u64 *pt,
                                                                         int64_t pstride, i64 *V, int comps, int L,
                                                                         int64_t count) {
     extern __shared__ u64 sm[];
-    const int c = blockIdx.x;
+    const int c = lbx<LOGN>();
     const PrimeInfo P = K.pi[L];
     const LastConst lc = K.last[L];
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         u64 x[16];
-        load16(at(in, b, c, L, LOGN) + threadIdx.x * 16, x);
+        load16(at(in, b, c, L, LOGN) + tpos<LOGN>(), x);
         if (pt) {
             u64 y[16];
-            load16(pt + b * pstride + ((int64_t)L << LOGN) + threadIdx.x * 16, y);
+            load16(pt + b * pstride + ((int64_t)L << LOGN) + tpos<LOGN>(), y);
 #pragma unroll
             for (int m = 0; m < 16; ++m) x[m] = mont_mul(x[m], y[m], P.p, P.pinv);
         }
@@ -29,11 +29,11 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_rescale
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_rescale_tail(Ctx K, heb_ct in, const u64 *pt,
+__global__ void ROW_BOUNDS(LOGN) k_rescale_tail(Ctx K, heb_ct in, const u64 *pt,
                                                                         int64_t pstride, const i64 *V, heb_ct out,
                                                                         int comps, int L, int64_t count) {
     extern __shared__ u64 sm[];
-    const int i = blockIdx.x, c = blockIdx.z;
+    const int i = lbx<LOGN>(), c = blockIdx.z;
     const PrimeInfo P = K.pi[i];
     const LevelConst C = K.lc[(size_t)L * K.num_rows + i];
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
@@ -42,23 +42,23 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_rescale
         fwd_any<LOGN>(K, i, P, sm,
                            [&](int j) { return signed_mul_const(__ldcg(src + j), C.beta_r.x, C.beta_r.y, P.p); }, y);
         u64 x[16];
-        load16(at(in, b, c, i, LOGN) + threadIdx.x * 16, x);
+        load16(at(in, b, c, i, LOGN) + tpos<LOGN>(), x);
         if (pt) {
             u64 z[16];
-            load16(pt + b * pstride + ((int64_t)i << LOGN) + threadIdx.x * 16, z);
+            load16(pt + b * pstride + ((int64_t)i << LOGN) + tpos<LOGN>(), z);
 #pragma unroll
             for (int m = 0; m < 16; ++m) x[m] = mont_mul(x[m], z[m], P.p, P.pinv);
         }
 #pragma unroll
         for (int m = 0; m < 16; ++m) x[m] = sub_mod(shoup(x[m], C.beta.x, C.beta.y, P.p), y[m], P.p);
-        store16(at(out, b, c, i, LOGN) + threadIdx.x * 16, x);
+        store16(at(out, b, c, i, LOGN) + tpos<LOGN>(), x);
     }
 }
 
 template <int LOGN>
 static int launch_rescale(heb_ctx *c, heb_ct in, const u64 *pt, int64_t pstride, heb_ct out, int64_t count, int comps,
                           int level, cudaStream_t st) {
-    constexpr int T = ntt::Shape<LOGN>::T;
+    constexpr int T = KT<LOGN>;
     constexpr size_t sm = smem_bytes<LOGN>();
     CUDA_TRY(prep_kernel(k_rescale_head<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_rescale_tail<LOGN>, sm));
@@ -71,11 +71,11 @@ static int launch_rescale(heb_ctx *c, heb_ct in, const u64 *pt, int64_t pstride,
         ib.data += b0 * in.ct_stride;
         ob.data += b0 * out.ct_stride;
         const u64 *pb = pt ? pt + b0 * pstride : nullptr;
-        { PROF("k_rescale_head", st, 8.0 * c->n * (2.0 * cnt * comps + (pt ? (pstride ? cnt : 1) : 0))); k_rescale_head<LOGN><<<dim3(comps, gdim(cnt)), T, sm, st>>>(kctx(c), ib, pb, pstride, (i64 *)V.p, comps,
-                                                                     level, cnt); }
+        { PROF("k_rescale_head", st, 8.0 * c->n * (2.0 * cnt * comps + (pt ? (pstride ? cnt : 1) : 0))); CUDA_TRY(launch_rows<LOGN>(k_rescale_head<LOGN>, dim3(dim3(comps, gdim(cnt))), KT<LOGN>, sm, st, kctx(c), ib, pb, pstride, (i64 *)V.p, comps,
+                                                                     level, cnt)); }
         LAUNCH_CHECK();
-        { PROF("k_rescale_tail", st, 8.0 * c->n * (cnt * comps * (1.0 + 2.0 * level) + (pt ? level * (pstride ? cnt : 1) : 0))); k_rescale_tail<LOGN><<<dim3(level, gdim(cnt), comps), T, sm, st>>>(kctx(c), ib, pb, pstride,
-                                                                            (const i64 *)V.p, ob, comps, level, cnt); }
+        { PROF("k_rescale_tail", st, 8.0 * c->n * (cnt * comps * (1.0 + 2.0 * level) + (pt ? level * (pstride ? cnt : 1) : 0))); CUDA_TRY(launch_rows<LOGN>(k_rescale_tail<LOGN>, dim3(dim3(level, gdim(cnt), comps)), KT<LOGN>, sm, st, kctx(c), ib, pb, pstride,
+                                                                            (const i64 *)V.p, ob, comps, level, cnt)); }
         LAUNCH_CHECK();
     }
     return HEB_OK;
@@ -103,15 +103,15 @@ extern "C" int heb_rescale(heb_ctx *c, heb_ct in, const uint64_t *pt, int64_t ps
 // since every step is an identity mod q_i.
 // =============================================================================
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_head(Ctx K, heb_ct src, int comp, i64 *D, int k,
+__global__ void ROW_BOUNDS(LOGN) k_ks_head(Ctx K, heb_ct src, int comp, i64 *D, int k,
                                                                    int64_t count) {
     extern __shared__ u64 sm[];
-    const int j = blockIdx.x;
+    const int j = lbx<LOGN>();
     const PrimeInfo P = K.pi[j];
     const LastConst lc = K.last[j];
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         u64 x[16];
-        load16(at(src, b, comp, j, LOGN) + threadIdx.x * 16, x);
+        load16(at(src, b, comp, j, LOGN) + tpos<LOGN>(), x);
         i64 *dst = D + (b * k + j) * (1 << LOGN);
         inv_any<LOGN>(K, j, P, sm, x, [&](int i, u64 v) { dst[i] = center(v, P.p); }, true);
     }
@@ -131,12 +131,12 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_head
 //                    (the centred digit is congruent to d2_t mod its own prime).
 // V layout: (count, k+1, k, N); slot (t, t) is unused.
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN))
+__global__ void ROW_BOUNDS(LOGN)
     k_ks_modup_ntt(Ctx K, const i64 *D, int k, u64 *V, int64_t count) {
     extern __shared__ u64 sm[];
     // blockIdx.x enumerates the k^2 (t, j) pairs with j != t: k-1 digits for each
     // ciphertext target t < k, then all k digits for the special prime (t = k)
-    const int x = blockIdx.x;
+    const int x = lbx<LOGN>();
     int t, j;
     if (x < k * (k - 1)) {
         t = x / (k - 1);
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN))
         const i64 *dj = D + (b * k + j) * n;
         u64 y[16];
         fwd_any<LOGN>(K, gt, P, sm, [&](int i) { return signed_mul_const(__ldcg(dj + i), P.rmod, P.rmod_s, P.p); }, y);
-        store16(V + ((b * (k + 1) + t) * k + j) * n + threadIdx.x * 16, y);
+        store16(V + ((b * (k + 1) + t) * k + j) * n + tpos<LOGN>(), y);
     }
 }
 
@@ -218,12 +218,12 @@ extern "C" int heb_prepare_switch_key(heb_ctx *c, const uint64_t *kb, const uint
 
 // which = 0: aP = center_P(INTT_P(acc_P)) ; which = 1: bL = INTT_L(acc_L + P d_L) (std form)
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_down_head(Ctx K, const u64 *acc, heb_ct d, int k,
+__global__ void ROW_BOUNDS(LOGN) k_ks_down_head(Ctx K, const u64 *acc, heb_ct d, int k,
                                                                         i64 *aP, u64 *bL, int64_t count) {
     extern __shared__ u64 sm[];
-    const int which = blockIdx.x, c = blockIdx.z;
+    const int which = lbx<LOGN>(), c = blockIdx.z;
     const int n = 1 << LOGN;
-    const int pos = threadIdx.x * 16;
+    const int pos = tpos<LOGN>();
     const int row = which == 0 ? K.num_rows - 1 : k - 1;
     const int arow = which == 0 ? k : k - 1;
     const PrimeInfo P = K.pi[row];
@@ -247,13 +247,13 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_down
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_down_rescale_tail(Ctx K, const u64 *acc, heb_ct d,
+__global__ void ROW_BOUNDS(LOGN) k_ks_down_rescale_tail(Ctx K, const u64 *acc, heb_ct d,
                                                                                 const i64 *aP, const u64 *bL, int k,
                                                                                 heb_ct out, int64_t count) {
     extern __shared__ u64 sm[];
-    const int i = blockIdx.x, c = blockIdx.z;
+    const int i = lbx<LOGN>(), c = blockIdx.z;
     const int n = 1 << LOGN;
-    const int pos = threadIdx.x * 16;
+    const int pos = tpos<LOGN>();
     const int L = k - 1;
     const PrimeInfo Pi = K.pi[i];
     const PrimeInfo PL = K.pi[L];
@@ -288,12 +288,12 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_down
 
 // ModDown without rescale (rotation): out_i = acc_i P^-1 - NTT_i(aP P^-1 R) [+ add0_i for c = 0]
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_down_tail(Ctx K, const u64 *acc, const i64 *aP, int k,
+__global__ void ROW_BOUNDS(LOGN) k_ks_down_tail(Ctx K, const u64 *acc, const i64 *aP, int k,
                                                                         heb_ct add0, heb_ct out, int64_t count) {
     extern __shared__ u64 sm[];
-    const int i = blockIdx.x, c = blockIdx.z;
+    const int i = lbx<LOGN>(), c = blockIdx.z;
     const int n = 1 << LOGN;
-    const int pos = threadIdx.x * 16;
+    const int pos = tpos<LOGN>();
     const PrimeInfo Pi = K.pi[i];
     const LevelConst Ci = K.lc[(size_t)(k - 1) * K.num_rows + i];
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ks_down
 template <int LOGN>
 static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *key, heb_ct d, heb_ct out,
                             int64_t count, int level, bool rescale, cudaStream_t st) {
-    constexpr int T = ntt::Shape<LOGN>::T;
+    constexpr int T = KT<LOGN>;
     constexpr size_t sm = smem_bytes<LOGN>();
     CUDA_TRY(prep_kernel(k_ks_head<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_ks_modup_ntt<LOGN>, sm));
@@ -344,7 +344,7 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
         dd.data += b0 * d.ct_stride;
         o.data += b0 * out.ct_stride;
         const unsigned gy = gdim(cnt);
-        { PROF("k_ks_head", st, 16.0 * n * cnt * k); k_ks_head<LOGN><<<dim3(k, gy), T, sm, st>>>(K, s, comp, (i64 *)sD.p, k, cnt); }
+        { PROF("k_ks_head", st, 16.0 * n * cnt * k); CUDA_TRY(launch_rows<LOGN>(k_ks_head<LOGN>, dim3(dim3(k, gy)), KT<LOGN>, sm, st, K, s, comp, (i64 *)sD.p, k, cnt)); }
         LAUNCH_CHECK();
         for (int64_t s0 = 0; s0 < cnt; s0 += sub) {
             const int64_t sc = std::min<int64_t>(sub, cnt - s0);
@@ -354,7 +354,7 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
             u64 *Ap = (u64 *)sA.p + s0 * 2 * (k + 1) * n;
             {
                 PROF("k_ks_modup_ntt", st, 16.0 * n * sc * k * k);
-                k_ks_modup_ntt<LOGN><<<dim3(k * k, gdim(sc)), T, sm, st>>>(K, Dp, k, (u64 *)sV.p, sc);
+                CUDA_TRY(launch_rows<LOGN>(k_ks_modup_ntt<LOGN>, dim3(dim3(k * k, gdim(sc))), KT<LOGN>, sm, st, K, Dp, k, (u64 *)sV.p, sc));
             }
             LAUNCH_CHECK();
             {
@@ -365,19 +365,19 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
             LAUNCH_CHECK();
         }
         if (rescale) {
-            { PROF("k_ks_down_head", st, 8.0 * n * cnt * 10.0); k_ks_down_head<LOGN><<<dim3(2, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
-                                                                 (u64 *)sL.p, cnt); }
+            { PROF("k_ks_down_head", st, 8.0 * n * cnt * 10.0); CUDA_TRY(launch_rows<LOGN>(k_ks_down_head<LOGN>, dim3(dim3(2, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
+                                                                 (u64 *)sL.p, cnt)); }
             LAUNCH_CHECK();
-            { PROF("k_ks_down_rescale_tail", st, 8.0 * n * cnt * 2.0 * (2 + 3 * (k - 1))); k_ks_down_rescale_tail<LOGN><<<dim3(k - 1, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, dd,
+            { PROF("k_ks_down_rescale_tail", st, 8.0 * n * cnt * 2.0 * (2 + 3 * (k - 1))); CUDA_TRY(launch_rows<LOGN>(k_ks_down_rescale_tail<LOGN>, dim3(dim3(k - 1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd,
                                                                              (const i64 *)sP.p, (const u64 *)sL.p, k,
-                                                                             o, cnt); }
+                                                                             o, cnt)); }
             LAUNCH_CHECK();
         } else {
-            { PROF("k_ks_down_head", st, 8.0 * n * cnt * 4.0); k_ks_down_head<LOGN><<<dim3(1, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
-                                                                 (u64 *)sL.p, cnt); }
+            { PROF("k_ks_down_head", st, 8.0 * n * cnt * 4.0); CUDA_TRY(launch_rows<LOGN>(k_ks_down_head<LOGN>, dim3(dim3(1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
+                                                                 (u64 *)sL.p, cnt)); }
             LAUNCH_CHECK();
-            { PROF("k_ks_down_tail", st, 8.0 * n * cnt * (2.0 + 5.0 * k)); k_ks_down_tail<LOGN><<<dim3(k, gy, 2), T, sm, st>>>(K, (const u64 *)sA.p, (const i64 *)sP.p, k, dd, o,
-                                                                 cnt); }
+            { PROF("k_ks_down_tail", st, 8.0 * n * cnt * (2.0 + 5.0 * k)); CUDA_TRY(launch_rows<LOGN>(k_ks_down_tail<LOGN>, dim3(dim3(k, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, (const i64 *)sP.p, k, dd, o,
+                                                                 cnt)); }
             LAUNCH_CHECK();
         }
     }

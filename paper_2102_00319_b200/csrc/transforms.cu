@@ -5,30 +5,32 @@
 // transforms
 // =============================================================================
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ntt_fwd(Ctx K, u64 *data, int64_t count, int row0,
+__global__ void ROW_BOUNDS(LOGN) k_ntt_fwd(Ctx K, u64 *data, int64_t count, int row0,
                                                                    int64_t bstride) {
     extern __shared__ u64 sm[];
-    const int r = blockIdx.x, prime = row0 + r;
+    const int r = lbx<LOGN>(), prime = row0 + r;
     const PrimeInfo P = K.pi[prime];
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         u64 *row = data + b * bstride + ((int64_t)r << LOGN);
         u64 y[16];
         fwd_any<LOGN>(K, prime, P, sm, [&](int i) { return __ldcg(row + i); }, y);
-        __syncthreads();  // all reads of `row` done before in-place writes
-        store16(row + threadIdx.x * 16, y);
+        // all reads of `row` (by both CTAs of a split row) done before in-place writes
+        if constexpr (Row<LOGN>::SPLIT) cooperative_groups::this_cluster().sync();
+        else __syncthreads();
+        store16(row + tpos<LOGN>(), y);
     }
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ntt_inv(Ctx K, u64 *data, int64_t count, int row0,
+__global__ void ROW_BOUNDS(LOGN) k_ntt_inv(Ctx K, u64 *data, int64_t count, int row0,
                                                                    int64_t bstride) {
     extern __shared__ u64 sm[];
-    const int r = blockIdx.x, prime = row0 + r;
+    const int r = lbx<LOGN>(), prime = row0 + r;
     const PrimeInfo P = K.pi[prime];
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         u64 *row = data + b * bstride + ((int64_t)r << LOGN);
         u64 x[16];
-        load16(row + threadIdx.x * 16, x);
+        load16(row + tpos<LOGN>(), x);
         inv_any<LOGN>(K, prime, P, sm, x, [&](int i, u64 v) { row[i] = v; }, false);
     }
 }
@@ -36,15 +38,15 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_ntt_inv
 template <int LOGN>
 static int launch_ntt(heb_ctx *c, uint64_t *data, int64_t count, int rows, int row0, int64_t bstride,
                       cudaStream_t st, bool inverse) {
-    constexpr int T = ntt::Shape<LOGN>::T;
+    constexpr int T = KT<LOGN>;
     constexpr size_t sm = smem_bytes<LOGN>();
     dim3 grid(rows, gdim(count));
     if (inverse) {
         CUDA_TRY(prep_kernel(k_ntt_inv<LOGN>, sm));
-        { PROF("k_ntt_inv", st, 16.0 * c->n * rows * count); k_ntt_inv<LOGN><<<grid, T, sm, st>>>(kctx(c), data, count, row0, bstride); }
+        { PROF("k_ntt_inv", st, 16.0 * c->n * rows * count); CUDA_TRY(launch_rows<LOGN>(k_ntt_inv<LOGN>, dim3(grid), KT<LOGN>, sm, st, kctx(c), data, count, row0, bstride)); }
     } else {
         CUDA_TRY(prep_kernel(k_ntt_fwd<LOGN>, sm));
-        { PROF("k_ntt_fwd", st, 16.0 * c->n * rows * count); k_ntt_fwd<LOGN><<<grid, T, sm, st>>>(kctx(c), data, count, row0, bstride); }
+        { PROF("k_ntt_fwd", st, 16.0 * c->n * rows * count); CUDA_TRY(launch_rows<LOGN>(k_ntt_fwd<LOGN>, dim3(grid), KT<LOGN>, sm, st, kctx(c), data, count, row0, bstride)); }
     }
     LAUNCH_CHECK();
     return HEB_OK;
@@ -65,17 +67,17 @@ extern "C" int heb_ntt_inv(heb_ctx *c, uint64_t *data, int64_t count, int rows, 
 
 // spread_centered + ntt_fwd_rows (ckks.py:120-126): signed coefficient -> (v mod p) * R, NTT
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_spread_ntt(Ctx K, const i64 *coeffs, int64_t count,
+__global__ void ROW_BOUNDS(LOGN) k_spread_ntt(Ctx K, const i64 *coeffs, int64_t count,
                                                                       u64 *out, int64_t ostride) {
     extern __shared__ u64 sm[];
-    const int r = blockIdx.x;
+    const int r = lbx<LOGN>();
     const PrimeInfo P = K.pi[r];
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         const i64 *src = coeffs + (b << LOGN);
         u64 y[16];
         fwd_any<LOGN>(K, r, P, sm,
                            [&](int i) { return signed_mul_const(__ldcg(src + i), P.rmod, P.rmod_s, P.p); }, y);
-        store16(out + b * ostride + ((int64_t)r << LOGN) + threadIdx.x * 16, y);
+        store16(out + b * ostride + ((int64_t)r << LOGN) + tpos<LOGN>(), y);
     }
 }
 
@@ -84,7 +86,7 @@ static int launch_spread(heb_ctx *c, const int64_t *coeffs, int64_t count, uint6
                          int64_t ostride, cudaStream_t st) {
     constexpr size_t sm = smem_bytes<LOGN>();
     CUDA_TRY(prep_kernel(k_spread_ntt<LOGN>, sm));
-    { PROF("k_spread_ntt", st, 8.0 * c->n * count * (1.0 + rows)); k_spread_ntt<LOGN><<<dim3(rows, gdim(count)), ntt::Shape<LOGN>::T, sm, st>>>(kctx(c), coeffs, count, out, ostride); }
+    { PROF("k_spread_ntt", st, 8.0 * c->n * count * (1.0 + rows)); CUDA_TRY(launch_rows<LOGN>(k_spread_ntt<LOGN>, dim3(dim3(rows, gdim(count))), KT<LOGN>, sm, st, kctx(c), coeffs, count, out, ostride)); }
     LAUNCH_CHECK();
     return HEB_OK;
 }
@@ -100,13 +102,13 @@ extern "C" int heb_spread_ntt(heb_ctx *c, const int64_t *coeffs, int64_t count, 
 // client side: encrypt / decrypt / key generation (ckks.py:135-273)
 // =============================================================================
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_encrypt(Ctx K, const i64 *v, const i64 *e0m, const i64 *e1,
+__global__ void ROW_BOUNDS(LOGN) k_encrypt(Ctx K, const i64 *v, const i64 *e0m, const i64 *e1,
                                                                    const u64 *pkb, const u64 *pka, heb_ct out,
                                                                    int64_t count) {
     extern __shared__ u64 sm[];
-    const int r = blockIdx.x;
+    const int r = lbx<LOGN>();
     const PrimeInfo P = K.pi[r];
-    const int n = 1 << LOGN, pos = threadIdx.x * 16;
+    const int n = 1 << LOGN, pos = tpos<LOGN>();
     const ulonglong2 *tw = tw_row<LOGN>(K, r);
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         auto spread = [&](const i64 *src) { return [=](int i) { return signed_mul_const(__ldcg(src + i), P.rmod, P.rmod_s, P.p); }; };
@@ -130,7 +132,7 @@ static int launch_encrypt(heb_ctx *c, const i64 *v, const i64 *e0m, const i64 *e
                           heb_ct out, int64_t count, int k, cudaStream_t st) {
     constexpr size_t sm = smem_bytes<LOGN>();
     CUDA_TRY(prep_kernel(k_encrypt<LOGN>, sm));
-    { PROF("k_encrypt", st, 8.0 * c->n * (3.0 * count + 2.0 * k + 2.0 * count * k)); k_encrypt<LOGN><<<dim3(k, gdim(count)), ntt::Shape<LOGN>::T, sm, st>>>(kctx(c), v, e0m, e1, pkb, pka, out, count); }
+    { PROF("k_encrypt", st, 8.0 * c->n * (3.0 * count + 2.0 * k + 2.0 * count * k)); CUDA_TRY(launch_rows<LOGN>(k_encrypt<LOGN>, dim3(dim3(k, gdim(count))), KT<LOGN>, sm, st, kctx(c), v, e0m, e1, pkb, pka, out, count)); }
     LAUNCH_CHECK();
     return HEB_OK;
 }
@@ -145,13 +147,13 @@ extern "C" int heb_encrypt(heb_ctx *c, const int64_t *v, const int64_t *e0m, con
 
 // decrypt rows 0/1: m = c1*s + c0 -> INTT -> std form
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_decrypt_rows(Ctx K, heb_ct ct, const u64 *s, u64 *tmp,
+__global__ void ROW_BOUNDS(LOGN) k_decrypt_rows(Ctx K, heb_ct ct, const u64 *s, u64 *tmp,
                                                                         int rows, int64_t count) {
     extern __shared__ u64 sm[];
-    const int r = blockIdx.x;
+    const int r = lbx<LOGN>();
     const PrimeInfo P = K.pi[r];
     const LastConst lc = K.last[r];
-    const int n = 1 << LOGN, pos = threadIdx.x * 16;
+    const int n = 1 << LOGN, pos = tpos<LOGN>();
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         u64 x[16], y[16], z[16];
         load16(at(ct, b, 1, r, LOGN) + pos, x);
@@ -194,8 +196,8 @@ static int launch_decrypt(heb_ctx *c, heb_ct ct, const u64 *s, i64 *coeffs, i64 
     Scratch tmp(st);
     CUDA_TRY(tmp.get(sizeof(u64) * (size_t)count * rows * c->n));
     CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(i64) * count, st));
-    { PROF("k_decrypt_rows", st, 8.0 * c->n * (3.0 * count * rows + rows)); k_decrypt_rows<LOGN><<<dim3(rows, gdim(count)), ntt::Shape<LOGN>::T, sm, st>>>(kctx(c), ct, s, (u64 *)tmp.p, rows,
-                                                                                    count); }
+    { PROF("k_decrypt_rows", st, 8.0 * c->n * (3.0 * count * rows + rows)); CUDA_TRY(launch_rows<LOGN>(k_decrypt_rows<LOGN>, dim3(dim3(rows, gdim(count))), KT<LOGN>, sm, st, kctx(c), ct, s, (u64 *)tmp.p, rows,
+                                                                                    count)); }
     LAUNCH_CHECK();
     { PROF("k_decrypt_finish", st, 8.0 * c->n * count * (rows + 1.0)); k_decrypt_finish<<<pw_grid(c->n, count), 256, 0, st>>>(kctx(c), (const u64 *)tmp.p, coeffs, (unsigned long long *)bad,
                                                             rows, count, c->log_n); }
@@ -212,12 +214,12 @@ extern "C" int heb_decrypt(heb_ctx *c, heb_ct ct, const uint64_t *s_eval, int64_
 
 // pk_b = e - a*s   (row r)
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_make_pk(Ctx K, const u64 *s, const u64 *a, const i64 *e,
+__global__ void ROW_BOUNDS(LOGN) k_make_pk(Ctx K, const u64 *s, const u64 *a, const i64 *e,
                                                                    u64 *pkb) {
     extern __shared__ u64 sm[];
-    const int r = blockIdx.x;
+    const int r = lbx<LOGN>();
     const PrimeInfo P = K.pi[r];
-    const int pos = threadIdx.x * 16;
+    const int pos = tpos<LOGN>();
     u64 E[16], x[16], y[16];
     fwd_any<LOGN>(K, r, P, sm,
                        [&](int i) { return signed_mul_const(__ldcg(e + i), P.rmod, P.rmod_s, P.p); }, E);
@@ -231,13 +233,13 @@ __global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_make_pk
 
 // kb[j][r] = e_j - a_j,r s_r  (+ (P mod q_j) R * target_j on r == j, applied with mont_mul)
 template <int LOGN>
-__global__ void __launch_bounds__(ntt::Shape<LOGN>::T, NTT_MINB(LOGN)) k_make_swk(Ctx K, const u64 *s, const u64 *target,
+__global__ void ROW_BOUNDS(LOGN) k_make_swk(Ctx K, const u64 *s, const u64 *target,
                                                                     const u64 *a, const i64 *e, u64 *kb) {
     extern __shared__ u64 sm[];
-    const int r = blockIdx.x, j = blockIdx.y;
+    const int r = lbx<LOGN>(), j = blockIdx.y;
     const int R = K.num_rows;
     const PrimeInfo P = K.pi[r];
-    const int pos = threadIdx.x * 16;
+    const int pos = tpos<LOGN>();
     const i64 *ej = e + ((size_t)j << LOGN);
     u64 E[16], x[16], y[16];
     fwd_any<LOGN>(K, r, P, sm,
@@ -261,7 +263,7 @@ template <int LOGN>
 static int launch_pk(heb_ctx *c, const u64 *s, const u64 *a, const i64 *e, u64 *pkb, int rows, cudaStream_t st) {
     constexpr size_t sm = smem_bytes<LOGN>();
     CUDA_TRY(prep_kernel(k_make_pk<LOGN>, sm));
-    { PROF("k_make_pk", st, 8.0 * c->n * (1.0 + 3.0 * rows)); k_make_pk<LOGN><<<rows, ntt::Shape<LOGN>::T, sm, st>>>(kctx(c), s, a, e, pkb); }
+    { PROF("k_make_pk", st, 8.0 * c->n * (1.0 + 3.0 * rows)); CUDA_TRY(launch_rows<LOGN>(k_make_pk<LOGN>, dim3(rows), KT<LOGN>, sm, st, kctx(c), s, a, e, pkb)); }
     LAUNCH_CHECK();
     return HEB_OK;
 }
@@ -270,7 +272,7 @@ static int launch_swk(heb_ctx *c, const u64 *s, const u64 *t, const u64 *a, cons
                       cudaStream_t st) {
     constexpr size_t sm = smem_bytes<LOGN>();
     CUDA_TRY(prep_kernel(k_make_swk<LOGN>, sm));
-    { PROF("k_make_swk", st, 8.0 * c->n * (digits + 4.0 * digits * c->num_rows)); k_make_swk<LOGN><<<dim3(c->num_rows, digits), ntt::Shape<LOGN>::T, sm, st>>>(kctx(c), s, t, a, e, kb); }
+    { PROF("k_make_swk", st, 8.0 * c->n * (digits + 4.0 * digits * c->num_rows)); CUDA_TRY(launch_rows<LOGN>(k_make_swk<LOGN>, dim3(dim3(c->num_rows, digits)), KT<LOGN>, sm, st, kctx(c), s, t, a, e, kb)); }
     LAUNCH_CHECK();
     return HEB_OK;
 }

@@ -219,3 +219,57 @@ def test_batched_layers_match_reference(golden, dev_s128, name, fused):
     assert be.counters.snapshot().__dict__ == g["counters"]
     dec = be.decrypt_batch(out, keys)
     assert np.allclose(dec[:, :8].T, np.array(g["decrypted_first8"]), atol=0, rtol=0)
+
+
+@pytest.mark.parametrize("logn", [15])
+def test_ntt_split_rows_match_oracle(logn):
+    """N = 2^15 rows run on a 2-CTA cluster (DSMEM cross-half stage)."""
+    from oracle import ckks_oracle as oc
+    from paper_2102_00319_b200.backend import DeviceContext, u64_to_dev, dev_to_u64
+    from paper_2102_00319_b200.chain import build_chain
+    from paper_2102_00319_b200.params import derive_params
+
+    n = 1 << logn
+    ch = build_chain(derive_params(2 * n, 200, 40, seed=1), 20)
+    ctx = DeviceContext(ch)
+    rng = np.random.default_rng(logn)
+    rows = ch.num_rows
+    x = np.stack([rng.integers(0, int(q), n, dtype=np.uint64) for q in ch.p])
+    ref = x.copy()
+    oc.ntt_fwd_rows(ref, ch.twiddles, ch.p, ch.p_inv)
+    d = u64_to_dev(np.stack([x, x, x]), ctx.device)
+    ctx.call("heb_ntt_fwd", d.data_ptr(), 3, rows, 0, rows * n, ctx.stream)
+    got = dev_to_u64(d)
+    assert all(np.array_equal(got[i], ref) for i in range(3))
+    ctx.call("heb_ntt_inv", d.data_ptr(), 3, rows, 0, rows * n, ctx.stream)
+    assert np.array_equal(dev_to_u64(d)[2], x)
+
+
+@pytest.mark.parametrize("m", [2**13, 2**15, 2**16])
+def test_ring_sweep_ops_match_oracle(m):
+    """Every payload op bit-exact vs the oracle at N = 4096, 16384 and 32768 (split rows)."""
+    from oracle.ckks_oracle import OracleBackend
+    from paper_2102_00319_b200.backend import B200Backend
+    from paper_2102_00319_b200.params import derive_params
+
+    params = derive_params(m, 220, 40, seed=3)
+    dev, ora = B200Backend(params, 20), OracleBackend(params, 20)
+    dk, ok = dev.keygen(galois_steps=(1,)), ora.keygen(galois_steps=(1,))
+    dev.set_eval_key(dk)
+    ora.set_eval_key(ok)
+    rng = np.random.default_rng(m)
+    x, y = rng.uniform(-1, 1, (2, dev.slots))
+
+    def same(a, b, what):
+        c0, c1 = dev.cipher_rows_host(a)
+        assert np.array_equal(c0, b.payload.c0) and np.array_equal(c1, b.payload.c1), what
+
+    dx, dy = dev.encrypt(x, dk, entropy=1), dev.encrypt(y, dk, entropy=2)
+    ox, oy = ora.encrypt(x, ok, entropy=1), ora.encrypt(y, ok, entropy=2)
+    same(dx, ox, "encrypt")
+    dm, om = dev.mul_ct_ct(dx, dy), ora.mul_ct_ct(ox, oy)
+    same(dm, om, "mul_ct_ct")
+    same(dev.mul_ct_pt(dx, y), ora.mul_ct_pt(ox, y), "mul_ct_pt")
+    same(dev.rotate(dx, 1), ora.rotate(ox, 1), "rotate")
+    same(dev.mul_ct_ct(dm, dm), ora.mul_ct_ct(om, om), "second level")
+    assert np.max(np.abs(dev.decrypt(dm, dk).values - x * y)) < 1e-4
