@@ -233,7 +233,7 @@ def run_gpu(args) -> None:
         name, (cnt, tot_ms, tot_bytes) = top
         achieved = tot_bytes / (tot_ms / 1e3) / 1e9
         traffic = ncu_traffic(name)
-        cpu = cpu_baseline(args) if (world == 1 and not args.skip_cpu) else None
+        cpu = cpu_baseline(args) if (world == 1 and not args.skip_cpu and args.config == "cfg2") else None
         path_rate = CFG2_PATH_BYTES_PER_BATCH * value / batch / 1e9 if args.config == "cfg2" else None
         line = {
             "metric": BASELINE_METRIC,
@@ -249,7 +249,7 @@ def run_gpu(args) -> None:
             "dtype": "u64",
             "data": "synthetic (seeded U[0,1] 28x28 pixels, N(0,0.1^2) weights; MNIST absent)",
             "config": {
-                "workload": f"{args.config}: encrypted CNN conv5x5x5/s2 -> x^2 -> sumpool2x2 -> FC180x10, "
+                "workload": f"{args.config}: encrypted CNN {' -> '.join(l.kind for l in net.layers)}, "
                             f"N={be.n}, {be.chain.num_levels} levels, {batch} images/GPU",
                 "batch_per_gpu": batch,
                 "ring_degree": be.n,
@@ -509,7 +509,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4"])
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-cfg1", action="store_true")
     args = ap.parse_args()

@@ -303,5 +303,77 @@ class LayerEvaluator:
         return x
 
 
+    # -- cells-mode sharding (sharding.py): one batch split over ranks -----------------
+    def run_cells_shard(self, enc: EncryptedNetworkBatch, x: CipherBatch, units) -> tuple:
+        """This rank's FC raw partials (out_dim, 3, k, N) over its (filter, pool row) units."""
+        from . import sharding as sh
+
+        net = enc.net
+        lay = sh.CellsLayout.of(net)
+        conv, act, dense = net.layers[0], net.layers[1], net.layers[4]
+        m, n = net.input_dims
+        C = conv.channels
+        p, q = conv.kernel
+        s = conv.stride
+        cells = sh.conv_cells(lay, units)
+        key = tuple(units)
+        taps = C * p * q
+
+        def build_conv():
+            ia, ib = [], []
+            for f, i, j in cells:
+                ia.append([c * m * n + (i * s + dp) * n + (j * s + dq) for c in range(C) for dp in range(p) for dq in range(q)])
+                ib.append([((f * C + c) * p + dp) * q + dq for c in range(C) for dp in range(p) for dq in range(q)])
+            return np.stack([np.array(ia), np.array(ib)])
+
+        idx = self._idx(("shard_conv", key), build_conv)
+        raw, lvl, scale, noise = self.dot(x, enc.weights[0], idx[0], idx[1], taps, len(cells))
+        y = self.finalize(raw, lvl, scale, noise)
+        if enc.biases[0] is not None:
+            bsel = self._idx(("shard_bias", key), lambda: np.array([f for f, _, _ in cells]))
+            bias = enc.biases[0]
+            gathered = self._empty(len(cells), 2, bias.k)
+            self.ctx.call("heb_gather", bias.desc(), bsel.data_ptr(), ct_desc(gathered), len(cells), 2, bias.k,
+                          self.ctx.stream)
+            y = self.add(y, CipherBatch(gathered, bias.level, bias.scale, bias.noise_bits))
+        y = self.square(y) if isinstance(act, Square) else self.poly_act(y, act)
+        pos = {c: t for t, c in enumerate(cells)}
+        pooled = sh.pooled_cells(lay, units)
+        pidx = self._idx(("shard_pool", key), lambda: np.array(
+            [[pos[(f, 2 * r + di, 2 * j + dj)] for di, dj in WINDOW_ORDER] for f, r, j in pooled]))
+        pool = self._empty(len(pooled), 2, y.k)
+        self.ctx.call("heb_sum_gather", y.desc(), pidx.data_ptr(), 4, ct_desc(pool), len(pooled), 2, y.k,
+                      self.ctx.stream)
+        self.be.counters.bump(ctct_add=3 * len(pooled))
+        pnoise = y.noise_bits
+        for _ in range(3):
+            pnoise = noise_sum(pnoise, y.noise_bits)
+        pooled_b = CipherBatch(pool, y.level, y.scale, pnoise)
+        dout = dense.out_dim
+
+        def build_fc():
+            ia = np.broadcast_to(np.arange(len(pooled))[None, :], (dout, len(pooled)))
+            flat = np.array([sh.flat_of(lay, f, r, j) for f, r, j in pooled])
+            ib = flat[None, :] * dout + np.arange(dout)[:, None]
+            return np.stack([ia, ib])
+
+        fidx = self._idx(("shard_fc", key), build_fc)
+        return self.dot(pooled_b, enc.weights[4], fidx[0], fidx[1], len(pooled), dout)
+
+    def finish_cells(self, enc: EncryptedNetworkBatch, parts: torch.Tensor, level: int, scale: Fraction,
+                     noise: float) -> CipherBatch:
+        """Add the gathered partials (world, out, 3, k, N) mod p, relinearise + rescale, bias."""
+        world, dout = parts.shape[0], parts.shape[1]
+        k = parts.shape[3]
+        flat = parts.reshape(world * dout, 3, k, self.be.n)
+        idx = self._idx(("combine", world, dout), lambda: np.array([[w * dout + r for w in range(world)] for r in range(dout)]))
+        raw = self._empty(dout, 3, k)
+        self.ctx.call("heb_sum_gather", ct_desc(flat), idx.data_ptr(), world, ct_desc(raw), dout, 3, k, self.ctx.stream)
+        self.be.counters.bump(ctct_add=dout * (world - 1))
+        y = self.finalize(raw, level, scale, noise + math.log2(world))
+        bias = enc.biases[4]
+        return self.add(y, bias) if bias is not None else y
+
+
 def bias_item(bias: CipherBatch, i: int) -> CipherBatch:
     return CipherBatch(bias.buf[i:i + 1], bias.level, bias.scale, bias.noise_bits)
