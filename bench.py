@@ -81,7 +81,7 @@ class Clocks:
         os.close(fd)
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "50",
                  "-i", str(self.device)], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -194,25 +194,25 @@ def run_gpu(args) -> None:
     launches = sum(v[0] for v in prof.values())
 
     # ---- end-to-end: host buffers through the public API -------------------------------
-    x_host = torch.empty(x.buf.shape, dtype=x.buf.dtype, pin_memory=True)
-    x_host.copy_(x.buf)
-    x_dev = torch.empty_like(x.buf)
-    x_in = layers.CipherBatch(x_dev, x.level, x.scale, x.noise_bits)
-    logits_host = torch.empty((out.count, 2, out.k, be.n), dtype=torch.int64, pin_memory=True)
-    for _ in range(max(1, args.warmup // 2)):
-        x_dev.copy_(x_host, non_blocking=True)
-        o = ev.run(enc, x_in)
-        logits_host.copy_(o.buf[:, :, : o.k], non_blocking=True)
+    # Every step copies its input ciphertexts from pinned host memory and its logits
+    # back; LayerEvaluator.run_stream overlaps the copy of batch s+1 with batch s.
+    x_hosts = [torch.empty(x.buf.shape, dtype=x.buf.dtype, pin_memory=True) for _ in range(2)]
+    for h in x_hosts:
+        h.copy_(x.buf)
+    logits_hosts = [torch.empty((out.count, 2, out.k, be.n), dtype=torch.int64, pin_memory=True)
+                    for _ in range(args.steps)]
+
+    def e2e_run(nsteps):
+        ev.run_stream(enc, [x_hosts[s % 2] for s in range(nsteps)], x.level, x.scale, x.noise_bits,
+                      logits_hosts[:nsteps], on_output=lambda s, o: gather(o))
+
+    e2e_run(min(args.steps, max(2, args.warmup)))
     torch.cuda.synchronize()
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        x_dev.copy_(x_host, non_blocking=True)
-        o = ev.run(enc, x_in)
-        gather(o)
-        logits_host.copy_(o.buf[:, :, : o.k], non_blocking=True)
+    e2e_run(args.steps)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -506,7 +506,7 @@ def run_reference(args) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4"])

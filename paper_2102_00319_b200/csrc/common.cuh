@@ -227,6 +227,27 @@ __device__ __forceinline__ void store16(u64 *__restrict__ dst, const u64 (&v)[16
 #define NTT_MINB_LL(LL) \
     (((65536 / NTT_REGS_PER_THREAD) >> ((LL) - 4)) > 32 ? 32 : (((65536 / NTT_REGS_PER_THREAD) >> ((LL) - 4)) < 1 ? 1 : ((65536 / NTT_REGS_PER_THREAD) >> ((LL) - 4))))
 #define NTT_MINB(LOGN) NTT_MINB_LL(Row<LOGN>::LL)
+// min CTAs/SM for a block of T threads at NTT_REGS_PER_THREAD registers
+#define NTT_MINB_T(T) \
+    ((65536 / NTT_REGS_PER_THREAD / (T)) > 32 ? 32 : ((65536 / NTT_REGS_PER_THREAD / (T)) < 1 ? 1 : (65536 / NTT_REGS_PER_THREAD / (T))))
+
+// E contiguous positions (E even): 16-byte vector load/store through L2
+template <int E>
+__device__ __forceinline__ void loadv(const u64 *__restrict__ src, u64 (&v)[E]) {
+    const ulonglong2 *s = reinterpret_cast<const ulonglong2 *>(src);
+#pragma unroll
+    for (int i = 0; i < E / 2; ++i) {
+        ulonglong2 t = __ldcg(s + i);
+        v[2 * i] = t.x;
+        v[2 * i + 1] = t.y;
+    }
+}
+template <int E>
+__device__ __forceinline__ void storev(u64 *__restrict__ dst, const u64 (&v)[E]) {
+    ulonglong2 *d = reinterpret_cast<ulonglong2 *>(dst);
+#pragma unroll
+    for (int i = 0; i < E / 2; ++i) __stcg(d + i, make_ulonglong2(v[2 * i], v[2 * i + 1]));
+}
 // launch bounds of a row kernel (E = 16 engine)
 #define ROW_BOUNDS(LOGN) __launch_bounds__(KT<LOGN>, NTT_MINB(LOGN))
 

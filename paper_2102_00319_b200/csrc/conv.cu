@@ -43,12 +43,64 @@ __global__ void __launch_bounds__(XC *SW, 2) k_conv_tensor(Ctx K, heb_ct A, heb_
         const int64_t widx = (int64_t)(f0 + fl) * taps + tap;
         const u64 *src = B.data + widx * B.ct_stride + roff;
         u64 *dst = wsm + ((size_t)(tap * FG + fl) * 2) * XC + xl;
-        dst[0] = src[0];
-        dst[XC] = src[B.comp_stride];
+        if (Pr.use_fp) {  // FP64 rows: stage the weights as doubles
+            dst[0] = (u64)__double_as_longlong(ntt::u2d(src[0]));
+            dst[XC] = (u64)__double_as_longlong(ntt::u2d(src[B.comp_stride]));
+        } else {
+            dst[0] = src[0];
+            dst[XC] = src[B.comp_stride];
+        }
     }
     __syncthreads();
 
     const int cells = om * on;
+    if (Pr.use_fp) {
+        // Rows with p < 2^42: every product reduced exactly on the FP64 pipe (6 ops),
+        // sums exact below 2^47; one R^-1 product per output restores the Montgomery
+        // factor of the reference's mont_mul accumulation.
+        const double pd = Pr.pd, pinvd = Pr.pinvd, rinv = (double)Pr.rinv;
+        const double *wd = reinterpret_cast<const double *>(wsm);
+        for (int cell = w; cell < cells; cell += SW) {
+            const int i = cell / on, j = cell % on;
+            double s0[FG], s1[FG], s2[FG];
+#pragma unroll
+            for (int fl = 0; fl < FG; ++fl) s0[fl] = s1[fl] = s2[fl] = 0.0;
+            for (int c = 0; c < C; ++c) {
+                for (int pp = 0; pp < P; ++pp) {
+                    const int64_t rowcell = (int64_t)c * m * n + (int64_t)(i * s + pp) * n + j * s;
+                    for (int qq = 0; qq < Q; ++qq) {
+                        const int tap = (c * P + pp) * Q + qq;
+                        const u64 *ap = A.data + (rowcell + qq) * A.ct_stride + roff;
+                        const double a0 = ntt::u2d(__ldg(ap)), a1 = ntt::u2d(__ldg(ap + A.comp_stride));
+                        const double sa = a0 + a1;
+                        const double *wt = wd + (size_t)(tap * FG) * 2 * XC + xl;
+#pragma unroll
+                        for (int fl = 0; fl < FG; ++fl) {
+                            if (fl < nf) {
+                                const double b0 = wt[(2 * fl) * XC], b1 = wt[(2 * fl + 1) * XC];
+                                s0[fl] += ntt::fmul(a0, b0, pd, pinvd);
+                                s2[fl] += ntt::fmul(a1, b1, pd, pinvd);
+                                s1[fl] += ntt::fmul(sa, b0 + b1, pd, pinvd);
+                            }
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int fl = 0; fl < FG; ++fl) {
+                if (fl < nf) {
+                    const double e0 = ntt::fmul(s0[fl], rinv, pd, pinvd);
+                    const double e2 = ntt::fmul(s2[fl], rinv, pd, pinvd);
+                    const double e1 = ntt::fmul(s1[fl], rinv, pd, pinvd) - e0 - e2;
+                    u64 *dp = D.data + ((int64_t)(f0 + fl) * cells + cell) * D.ct_stride + roff;
+                    dp[0] = ntt::fcanon(e0, pd, pinvd);
+                    dp[D.comp_stride] = ntt::fcanon(e1, pd, pinvd);
+                    dp[2 * D.comp_stride] = ntt::fcanon(e2, pd, pinvd);
+                }
+            }
+        }
+        return;
+    }
     for (int cell = w; cell < cells; cell += SW) {
         const int i = cell / on, j = cell % on;
         acc4 s0[FG], s1[FG], s2[FG];

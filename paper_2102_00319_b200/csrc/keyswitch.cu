@@ -135,16 +135,29 @@ __global__ void ROW_BOUNDS(LOGN)
     k_ks_modup_ntt(Ctx K, const i64 *D, int k, u64 *V, int64_t count) {
     extern __shared__ u64 sm[];
     // blockIdx.x enumerates the k^2 (t, j) pairs with j != t: k-1 digits for each
-    // ciphertext target t < k, then all k digits for the special prime (t = k)
-    const int x = lbx<LOGN>();
+    // ciphertext target t < k, then all k digits for the special prime (t = k).
+    // Targets 0 (base prime) and k (special prime) are the wide primes that run on
+    // the integer engine; their 2k-1 pairs are spread evenly through the launch order
+    // so that co-resident CTAs keep both the IMAD and the DFMA pipes busy.
+    const int xi = lbx<LOGN>();
+    const int total = k * k, nwide = 2 * k - 1;
+    const int wide_before = (int)(((long)xi * nwide) / total);
+    const bool is_wide = ((long)(xi + 1) * nwide) / total != wide_before;
     int t, j;
-    if (x < k * (k - 1)) {
-        t = x / (k - 1);
-        j = x % (k - 1);
+    if (is_wide) {  // wide pair #wide_before: t = 0 (j = 1..k-1) then t = k (j = 0..k-1)
+        const int w = wide_before;
+        if (w < k - 1) {
+            t = 0;
+            j = w + 1;
+        } else {
+            t = k;
+            j = w - (k - 1);
+        }
+    } else {  // narrow pair #(xi - wide_before): t = 1..k-1, j != t
+        const int q = xi - wide_before;
+        t = 1 + q / (k - 1);
+        j = q % (k - 1);
         j += (j >= t);
-    } else {
-        t = k;
-        j = x - k * (k - 1);
     }
     const int gt = t < k ? t : K.num_rows - 1;
     const PrimeInfo P = K.pi[gt];
@@ -167,17 +180,70 @@ __global__ void k_ks_modup_mac(Ctx K, heb_ct src, int comp, const u64 *V, const 
     const PrimeInfo P = K.pi[gt];
     const u64 p2 = 2 * P.p;
     if (x >= n) return;
-    for (int64_t b = blockIdx.z; b < count; b += gridDim.z) {
-        u64 s0 = 0, s1 = 0;
+    if (P.use_fp) {
+        // FP64 rows: the prepared key holds w as doubles (b part then a part), products
+        // are exact FP64 modular products, sums stay exact below 2^47.  Each thread
+        // serves MI items so every key word read from L2 is used MI times.
+        constexpr int MI = 1;
+        for (int64_t b0 = (int64_t)blockIdx.z * MI; b0 < count; b0 += (int64_t)gridDim.z * MI) {
+            const int nb = (int)(count - b0 < MI ? count - b0 : MI);
+            double s0[MI], s1[MI];
+#pragma unroll
+            for (int g = 0; g < MI; ++g) s0[g] = s1[g] = 0.0;
+            for (int j = 0; j < k; ++j) {
+                const double *kd = reinterpret_cast<const double *>(key + (((size_t)j * K.num_rows + gt) * 2) * n);
+                const double kb = __ldg(kd + x), ka = __ldg(kd + n + x);
+#pragma unroll
+                for (int g = 0; g < MI; ++g) {
+                    if (g < nb) {
+                        const int64_t b = b0 + g;
+                        const u64 v = (j == t) ? __ldcg(at(src, b, comp, j, logn) + x)
+                                               : __ldcg(V + ((b * (k + 1) + t) * k + j) * n + x);
+                        const double vd = ntt::u2d(v);
+                        s0[g] += ntt::fmul(vd, kb, P.pd, P.pinvd);
+                        s1[g] += ntt::fmul(vd, ka, P.pd, P.pinvd);
+                    }
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < MI; ++g) {
+                if (g < nb) {
+                    const int64_t b = b0 + g;
+                    __stcg(acc + ((b * 2 + 0) * (k + 1) + t) * n + x, ntt::fcanon(s0[g], P.pd, P.pinvd));
+                    __stcg(acc + ((b * 2 + 1) * (k + 1) + t) * n + x, ntt::fcanon(s1[g], P.pd, P.pinvd));
+                }
+            }
+        }
+        return;
+    }
+    constexpr int MI = 1;
+    for (int64_t b0 = (int64_t)blockIdx.z * MI; b0 < count; b0 += (int64_t)gridDim.z * MI) {
+        const int nb = (int)(count - b0 < MI ? count - b0 : MI);
+        u64 s0[MI], s1[MI];
+#pragma unroll
+        for (int g = 0; g < MI; ++g) s0[g] = s1[g] = 0;
         for (int j = 0; j < k; ++j) {
-            const u64 v = (j == t) ? __ldcg(at(src, b, comp, j, logn) + x) : __ldcg(V + ((b * (k + 1) + t) * k + j) * n + x);
             const ulonglong2 *kb = key + (((size_t)j * K.num_rows + gt) * 2) * n + x;
             const ulonglong2 wb = __ldg(kb), wa = __ldg(kb + n);
-            s0 = csub(s0 + shoup_lazy(v, wb.x, wb.y, P.p), p2);
-            s1 = csub(s1 + shoup_lazy(v, wa.x, wa.y, P.p), p2);
+#pragma unroll
+            for (int g = 0; g < MI; ++g) {
+                if (g < nb) {
+                    const int64_t b = b0 + g;
+                    const u64 v = (j == t) ? __ldcg(at(src, b, comp, j, logn) + x)
+                                           : __ldcg(V + ((b * (k + 1) + t) * k + j) * n + x);
+                    s0[g] = csub(s0[g] + shoup_lazy(v, wb.x, wb.y, P.p), p2);
+                    s1[g] = csub(s1[g] + shoup_lazy(v, wa.x, wa.y, P.p), p2);
+                }
+            }
         }
-        __stcg(acc + ((b * 2 + 0) * (k + 1) + t) * n + x, csub(s0, P.p));
-        __stcg(acc + ((b * 2 + 1) * (k + 1) + t) * n + x, csub(s1, P.p));
+#pragma unroll
+        for (int g = 0; g < MI; ++g) {
+            if (g < nb) {
+                const int64_t b = b0 + g;
+                __stcg(acc + ((b * 2 + 0) * (k + 1) + t) * n + x, csub(s0[g], P.p));
+                __stcg(acc + ((b * 2 + 1) * (k + 1) + t) * n + x, csub(s1[g], P.p));
+            }
+        }
     }
 }
 
@@ -191,9 +257,14 @@ __global__ void k_prep_key(Ctx K, const u64 *kb, const u64 *ka, ulonglong2 *out,
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const size_t src = ((size_t)j * K.num_rows + r) * n + i;
         ulonglong2 *dst = out + (((size_t)j * K.num_rows + r) * 2) * n + i;
+        double *dstd = reinterpret_cast<double *>(out + (((size_t)j * K.num_rows + r) * 2) * n) + i;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             const u64 w = mont_mul(c == 0 ? kb[src] : ka[src], 1, P.p, P.pinv);
+            if (P.use_fp) {  // FP64 rows: w as a double, b part then a part
+                dstd[(size_t)c * n] = (double)w;
+                continue;
+            }
             u64 q = __umul64hi(w, P.rmod_s);
             const u64 rem = w * P.rmod - q * P.p;
             q += rem >= P.p;

@@ -4,34 +4,39 @@
 // =============================================================================
 // transforms
 // =============================================================================
+#ifndef PLAIN_E
+#define PLAIN_E 16
+#endif
 template <int LOGN>
-__global__ void ROW_BOUNDS(LOGN) k_ntt_fwd(Ctx K, u64 *data, int64_t count, int row0,
-                                                                   int64_t bstride) {
+__global__ void __launch_bounds__((KT<LOGN, PLAIN_E>), NTT_MINB_T((KT<LOGN, PLAIN_E>)))
+    k_ntt_fwd(Ctx K, u64 *data, int64_t count, int row0, int64_t bstride) {
+    constexpr int E = PLAIN_E;
     extern __shared__ u64 sm[];
     const int r = lbx<LOGN>(), prime = row0 + r;
     const PrimeInfo P = K.pi[prime];
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         u64 *row = data + b * bstride + ((int64_t)r << LOGN);
-        u64 y[16];
-        fwd_any<LOGN>(K, prime, P, sm, [&](int i) { return __ldcg(row + i); }, y);
+        u64 y[E];
+        fwd_any<LOGN, E>(K, prime, P, sm, [&](int i) { return __ldcg(row + i); }, y);
         // all reads of `row` (by both CTAs of a split row) done before in-place writes
         if constexpr (Row<LOGN>::SPLIT) cooperative_groups::this_cluster().sync();
         else __syncthreads();
-        store16(row + tpos<LOGN>(), y);
+        storev(row + tpos<LOGN, E>(), y);
     }
 }
 
 template <int LOGN>
-__global__ void ROW_BOUNDS(LOGN) k_ntt_inv(Ctx K, u64 *data, int64_t count, int row0,
-                                                                   int64_t bstride) {
+__global__ void __launch_bounds__((KT<LOGN, PLAIN_E>), NTT_MINB_T((KT<LOGN, PLAIN_E>)))
+    k_ntt_inv(Ctx K, u64 *data, int64_t count, int row0, int64_t bstride) {
+    constexpr int E = PLAIN_E;
     extern __shared__ u64 sm[];
     const int r = lbx<LOGN>(), prime = row0 + r;
     const PrimeInfo P = K.pi[prime];
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         u64 *row = data + b * bstride + ((int64_t)r << LOGN);
-        u64 x[16];
-        load16(row + tpos<LOGN>(), x);
-        inv_any<LOGN>(K, prime, P, sm, x, [&](int i, u64 v) { row[i] = v; }, false);
+        u64 x[E];
+        loadv(row + tpos<LOGN, E>(), x);
+        inv_any<LOGN, E>(K, prime, P, sm, x, [&](int i, u64 v) { row[i] = v; }, false);
     }
 }
 
@@ -43,10 +48,10 @@ static int launch_ntt(heb_ctx *c, uint64_t *data, int64_t count, int rows, int r
     dim3 grid(rows, gdim(count));
     if (inverse) {
         CUDA_TRY(prep_kernel(k_ntt_inv<LOGN>, sm));
-        { PROF("k_ntt_inv", st, 16.0 * c->n * rows * count); CUDA_TRY(launch_rows<LOGN>(k_ntt_inv<LOGN>, dim3(grid), KT<LOGN>, sm, st, kctx(c), data, count, row0, bstride)); }
+        { PROF("k_ntt_inv", st, 16.0 * c->n * rows * count); CUDA_TRY(launch_rows<LOGN>(k_ntt_inv<LOGN>, dim3(grid), KT<LOGN, PLAIN_E>, sm, st, kctx(c), data, count, row0, bstride)); }
     } else {
         CUDA_TRY(prep_kernel(k_ntt_fwd<LOGN>, sm));
-        { PROF("k_ntt_fwd", st, 16.0 * c->n * rows * count); CUDA_TRY(launch_rows<LOGN>(k_ntt_fwd<LOGN>, dim3(grid), KT<LOGN>, sm, st, kctx(c), data, count, row0, bstride)); }
+        { PROF("k_ntt_fwd", st, 16.0 * c->n * rows * count); CUDA_TRY(launch_rows<LOGN>(k_ntt_fwd<LOGN>, dim3(grid), KT<LOGN, PLAIN_E>, sm, st, kctx(c), data, count, row0, bstride)); }
     }
     LAUNCH_CHECK();
     return HEB_OK;

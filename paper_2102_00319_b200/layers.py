@@ -303,6 +303,43 @@ class LayerEvaluator:
         return x
 
 
+    # -- serving: host batches in, host logits out, copies overlapped with compute -----
+    def run_stream(self, enc: EncryptedNetworkBatch, host_inputs, level: int, scale: Fraction, noise: float,
+                   host_outputs, on_output=None) -> None:
+        """Evaluate a sequence of pinned host input batches ((B, 2, K, N) int64 tensors).
+
+        The host->device copy of batch s+1 runs on a copy stream while batch s is
+        evaluated; the logits of every batch are copied back into ``host_outputs[s]``
+        (pinned, (out, 2, k, N)).  Two device input buffers are rotated; events order
+        buffer reuse.  Returns after enqueueing (synchronise the current stream to wait).
+        """
+        compute = torch.cuda.current_stream(self.be.dev)
+        copy = torch.cuda.Stream(self.be.dev)
+        bufs = [torch.empty_like(host_inputs[0], device=self.be.dev) for _ in range(2)]
+        copied = [torch.cuda.Event() for _ in range(2)]
+        consumed = [torch.cuda.Event() for _ in range(2)]
+
+        def stage(s):
+            slot = s % 2
+            with torch.cuda.stream(copy):
+                if s >= 2:
+                    copy.wait_event(consumed[slot])
+                bufs[slot].copy_(host_inputs[s], non_blocking=True)
+                copied[slot].record(copy)
+
+        if host_inputs:
+            stage(0)
+        for s in range(len(host_inputs)):
+            if s + 1 < len(host_inputs):
+                stage(s + 1)
+            slot = s % 2
+            compute.wait_event(copied[slot])
+            out = self.run(enc, CipherBatch(bufs[slot], level, scale, noise))
+            consumed[slot].record(compute)
+            host_outputs[s].copy_(out.buf[:, :, : out.k], non_blocking=True)
+            if on_output is not None:
+                on_output(s, out)
+
     # -- cells-mode sharding (sharding.py): one batch split over ranks -----------------
     def run_cells_shard(self, enc: EncryptedNetworkBatch, x: CipherBatch, units) -> tuple:
         """This rank's FC raw partials (out_dim, 3, k, N) over its (filter, pool row) units."""
