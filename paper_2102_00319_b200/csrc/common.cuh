@@ -110,7 +110,10 @@ static inline Ctx kctx(const heb_ctx *c) {
 // holds after a forward transform, KT for their block size.
 template <int LOGN>
 struct Row {
-    static constexpr bool SPLIT = LOGN > 14;
+#ifndef SPLIT_MIN_LOGN
+#define SPLIT_MIN_LOGN 15
+#endif
+    static constexpr bool SPLIT = LOGN >= SPLIT_MIN_LOGN;
     static constexpr int LL = SPLIT ? LOGN - 1 : LOGN;  // residues per CTA = 2^LL
     static constexpr int N = 1 << LOGN;
 };

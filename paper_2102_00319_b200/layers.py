@@ -97,6 +97,7 @@ class LayerEvaluator:
         self.fused_conv = fused_conv
         self._idx_cache: dict = {}
         self._unique: dict = {}
+        self._streams: dict = {}
 
     # -- primitives -------------------------------------------------------------------
     def _idx(self, key, builder) -> torch.Tensor:
@@ -304,41 +305,66 @@ class LayerEvaluator:
 
 
     # -- serving: host batches in, host logits out, copies overlapped with compute -----
+    def _pipeline_streams(self, kind: str, count: int) -> list:
+        """Persistent per-pipeline streams (the caching allocator keeps per-stream pools,
+        so reusing streams keeps steady-state steps free of fresh device allocations)."""
+        pool = self._streams.setdefault(kind, [])
+        while len(pool) < count:
+            pool.append(torch.cuda.Stream(self.be.dev))
+        return pool[:count]
+
     def run_stream(self, enc: EncryptedNetworkBatch, host_inputs, level: int, scale: Fraction, noise: float,
-                   host_outputs, on_output=None) -> None:
+                   host_outputs, on_output=None, pipelines: int = 2) -> None:
         """Evaluate a sequence of pinned host input batches ((B, 2, K, N) int64 tensors).
 
-        The host->device copy of batch s+1 runs on a copy stream while batch s is
-        evaluated; the logits of every batch are copied back into ``host_outputs[s]``
-        (pinned, (out, 2, k, N)).  Two device input buffers are rotated; events order
-        buffer reuse.  Returns after enqueueing (synchronise the current stream to wait).
+        Batches are dealt round-robin to ``pipelines`` independent pipelines, each with
+        its own device input buffer, copy stream and compute stream: the host->device
+        copy of one pipeline's next batch overlaps the other pipelines' evaluation, and
+        the pipelines' kernels fill each other's tails on the SMs.  The logits of batch
+        s are copied back into ``host_outputs[s]`` (pinned, (out, 2, k, N)).  On return
+        the caller's current stream is ordered after all the work.
         """
-        compute = torch.cuda.current_stream(self.be.dev)
-        copy = torch.cuda.Stream(self.be.dev)
-        bufs = [torch.empty_like(host_inputs[0], device=self.be.dev) for _ in range(2)]
-        copied = [torch.cuda.Event() for _ in range(2)]
-        consumed = [torch.cuda.Event() for _ in range(2)]
-
-        def stage(s):
-            slot = s % 2
-            with torch.cuda.stream(copy):
-                if s >= 2:
-                    copy.wait_event(consumed[slot])
-                bufs[slot].copy_(host_inputs[s], non_blocking=True)
-                copied[slot].record(copy)
-
-        if host_inputs:
-            stage(0)
+        caller = torch.cuda.current_stream(self.be.dev)
+        P = max(1, pipelines)
+        comp = self._pipeline_streams("compute", P)
+        copy = self._pipeline_streams("copy", P)
+        for st in comp + copy:
+            st.wait_stream(caller)
+        bufs = [torch.empty_like(host_inputs[0], device=self.be.dev) for _ in range(P)]
+        copied = [torch.cuda.Event() for _ in range(P)]
+        consumed = [torch.cuda.Event() for _ in range(P)]
         for s in range(len(host_inputs)):
-            if s + 1 < len(host_inputs):
-                stage(s + 1)
-            slot = s % 2
-            compute.wait_event(copied[slot])
-            out = self.run(enc, CipherBatch(bufs[slot], level, scale, noise))
-            consumed[slot].record(compute)
-            host_outputs[s].copy_(out.buf[:, :, : out.k], non_blocking=True)
-            if on_output is not None:
-                on_output(s, out)
+            p = s % P
+            with torch.cuda.stream(copy[p]):
+                if s >= P:
+                    copy[p].wait_event(consumed[p])
+                bufs[p].copy_(host_inputs[s], non_blocking=True)
+                copied[p].record(copy[p])
+            with torch.cuda.stream(comp[p]):
+                comp[p].wait_event(copied[p])
+                out = self.run(enc, CipherBatch(bufs[p], level, scale, noise))
+                consumed[p].record(comp[p])
+                host_outputs[s].copy_(out.buf[:, :, : out.k], non_blocking=True)
+                if on_output is not None:
+                    on_output(s, out)
+        for st in comp + copy:
+            caller.wait_stream(st)
+
+    def run_many(self, enc: EncryptedNetworkBatch, x: CipherBatch, steps: int, pipelines: int = 2,
+                 on_output=None) -> None:
+        """Evaluate ``steps`` device-resident batches over ``pipelines`` concurrent streams."""
+        caller = torch.cuda.current_stream(self.be.dev)
+        P = max(1, pipelines)
+        comp = self._pipeline_streams("compute", P)
+        for st in comp:
+            st.wait_stream(caller)
+        for s in range(steps):
+            with torch.cuda.stream(comp[s % P]):
+                out = self.run(enc, x)
+                if on_output is not None:
+                    on_output(s, out)
+        for st in comp:
+            caller.wait_stream(st)
 
     # -- cells-mode sharding (sharding.py): one batch split over ranks -----------------
     def run_cells_shard(self, enc: EncryptedNetworkBatch, x: CipherBatch, units) -> tuple:
