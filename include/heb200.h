@@ -72,6 +72,11 @@ int heb_ntt_fwd(heb_ctx *ctx, uint64_t *data, int64_t count, int rows, int row0,
                 void *stream);
 int heb_ntt_inv(heb_ctx *ctx, uint64_t *data, int64_t count, int rows, int row0, int64_t block_stride,
                 void *stream);
+/* Serialization transforms (ckks.py:393-408), in place over rows 0..rows-1:
+ * eval_to_coeff = ntt_inv_rows + from_mont_rows (Montgomery eval rows -> standard-form
+ * coefficients, the reference's payload format); coeff_to_eval = to_mont_rows + ntt_fwd_rows. */
+int heb_eval_to_coeff(heb_ctx *ctx, uint64_t *data, int64_t count, int rows, int64_t block_stride, void *stream);
+int heb_coeff_to_eval(heb_ctx *ctx, uint64_t *data, int64_t count, int rows, int64_t block_stride, void *stream);
 /* Centered int64 coefficients (count, N) -> evaluation rows 0..rows-1 (Montgomery).
  * Restates spread_centered + ntt_fwd_rows (ckks.py:120-126); rows = num_rows gives
  * every chain row including the special prime (keygen, ckks.py:128-129). */

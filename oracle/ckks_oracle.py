@@ -33,6 +33,7 @@ from __future__ import annotations
 import ctypes
 import itertools
 import os
+import struct
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 from fractions import Fraction
@@ -41,7 +42,7 @@ import numpy as np
 
 from paper_2102_00319_b200 import hostmath as hm
 from paper_2102_00319_b200.chain import ModulusChain
-from paper_2102_00319_b200.errors import DecryptionOutOfRange
+from paper_2102_00319_b200.errors import DecryptionOutOfRange, FingerprintMismatch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
@@ -496,3 +497,41 @@ class OracleBackend(HEBackend):
 
     def _rotate_impl(self, ct, galois):
         return _Cipher(*self.o.rotate((ct.payload.c0, ct.payload.c1), self._galois_keys[galois], galois))
+
+    # serialization hooks (ckks.py:393-436): INTT + from_mont out, to_mont + NTT in
+    def cipher_payload_bytes(self, ct) -> bytes:
+        ch, k = self.chain, ct.level + 1
+        parts = [struct.pack("<II", k, self.n)]
+        for comp in (ct.payload.c0, ct.payload.c1):
+            buf = np.ascontiguousarray(comp[:k], dtype=np.uint64).copy()
+            ntt_inv_rows(buf, ch.twiddles[:k], ch.n_inv[:k], ch.p[:k], ch.p_inv[:k])
+            from_mont_rows(buf, ch.p[:k], ch.p_inv[:k])
+            parts.append(buf.astype("<u8").tobytes())
+        return b"".join(parts)
+
+    def cipher_from_payload(self, data: bytes, level: int, scale, noise_bits: float):
+        ch = self.chain
+        k, n = struct.unpack_from("<II", data, 0)
+        if n != self.n or k != level + 1:
+            raise FingerprintMismatch("ciphertext payload does not match parameters")
+        comps = []
+        for c in range(2):
+            buf = np.frombuffer(data, dtype="<u8", count=k * n, offset=8 + c * k * n * 8).reshape(k, n).astype(np.uint64)
+            out = np.empty_like(buf)
+            scalar_mul_rows(buf, ch.r2[:k], ch.p[:k], ch.p_inv[:k], out)
+            ntt_fwd_rows(out, ch.twiddles[:k], ch.p[:k], ch.p_inv[:k])
+            comps.append(out)
+        return self._cipher(_Cipher(*comps), level, Fraction(scale), noise_bits)
+
+    def key_payload_bytes(self, key) -> dict:
+        """ckks.py:456-466 (the three roles share one OKeys bundle here)."""
+        from paper_2102_00319_b200.serialization import pack_array
+
+        parts = {}
+        if key.secret is not None:
+            parts["secret"] = pack_array(key.secret.s_eval)
+        if key.public is not None:
+            parts["public"] = pack_array(key.public.pk_b) + pack_array(key.public.pk_a)
+        if key.evaluation is not None:
+            parts["evaluation"] = pack_array(key.evaluation.evk_b) + pack_array(key.evaluation.evk_a)
+        return parts

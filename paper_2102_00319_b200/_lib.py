@@ -44,6 +44,8 @@ SIGNATURES: dict[str, list] = {
     "heb_ntt_fwd": [_P, _P, _L, _I, _I, _L, _P],
     "heb_ntt_inv": [_P, _P, _L, _I, _I, _L, _P],
     "heb_spread_ntt": [_P, _P, _L, _P, _I, _L, _P],
+    "heb_eval_to_coeff": [_P, _P, _L, _I, _L, _P],
+    "heb_coeff_to_eval": [_P, _P, _L, _I, _L, _P],
     "heb_add": [_P, _CT, _CT, _CT, _L, _I, _I, _P],
     "heb_add_plain": [_P, _CT, _P, _L, _CT, _L, _I, _P],
     "heb_tensor": [_P, _CT, _CT, _CT, _L, _I, _I, _P],

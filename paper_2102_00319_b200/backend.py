@@ -19,6 +19,7 @@ evaluator in ``layers.py``.
 from __future__ import annotations
 
 import itertools
+import struct
 import threading
 from dataclasses import dataclass
 from fractions import Fraction
@@ -27,8 +28,9 @@ import numpy as np
 
 from . import _lib
 from . import hostmath as hm
+from . import serialization as ser
 from .contract import CipherVec, HEBackend, KeyMaterial, PlainVec, RawProduct
-from .errors import DecryptionOutOfRange, DeviceError
+from .errors import DecryptionOutOfRange, DeviceError, FingerprintMismatch, HecnnError
 from .params import HEParams
 
 try:
@@ -189,6 +191,7 @@ class B200Backend(HEBackend):
     """CKKS on B200: reference-compatible payload math executed by libheb200."""
 
     name = "b200"
+    wire_name = "ckks"  # payload format and math are the reference CKKS backend's (serialization.py)
 
     def __init__(self, params: HEParams, base_extra_bits: int | None = None, device: int = 0):
         super().__init__(params, base_extra_bits)
@@ -408,6 +411,94 @@ class B200Backend(HEBackend):
                          noise_bits: float = float("-inf")) -> CipherVec:
         buf = u64_to_dev(np.stack([c0, c1]), self.dev)
         return self._cipher(DevCipher(buf, level + 1), level, Fraction(scale), noise_bits)
+
+    # -- serialization hooks (ckks.py:389-483) ----------------------------------------------
+    # The payload format is the reference's: "<II" (k, N) then c0 and c1 as k x N
+    # little-endian u64 standard-form coefficients.  Conversion runs on the device
+    # (heb_eval_to_coeff / heb_coeff_to_eval) over whole batches in one launch.
+    def _rows_to_coeffs(self, rows: "torch.Tensor") -> np.ndarray:
+        """(..., k, N) Montgomery eval rows -> host (..., k, N) coefficient words."""
+        k = rows.shape[-2]
+        buf = rows.contiguous().clone() if rows.is_contiguous() else rows.contiguous()
+        count = buf.numel() // (k * self.n)
+        self.ctx.call("heb_eval_to_coeff", buf.data_ptr(), count, k, k * self.n, self.ctx.stream)
+        return dev_to_u64(buf)
+
+    def _coeffs_to_rows_dev(self, coeffs: np.ndarray) -> "torch.Tensor":
+        k = coeffs.shape[-2]
+        buf = u64_to_dev(coeffs, self.dev)
+        count = buf.numel() // (k * self.n)
+        self.ctx.call("heb_coeff_to_eval", buf.data_ptr(), count, k, k * self.n, self.ctx.stream)
+        return buf
+
+    def _payload_head(self, data: bytes, level: int) -> int:
+        k, n = struct.unpack_from("<II", data, 0)
+        if n != self.n or k != level + 1:
+            raise FingerprintMismatch("ciphertext payload does not match parameters")
+        if len(data) < 8 + 2 * k * n * 8:
+            raise HecnnError("truncated ciphertext payload")
+        return k
+
+    def cipher_payload_bytes(self, ct: CipherVec) -> bytes:
+        k = ct.level + 1
+        words = self._rows_to_coeffs(ct.payload.rows())
+        return struct.pack("<II", k, self.n) + np.ascontiguousarray(words, dtype="<u8").tobytes()
+
+    def cipher_from_payload(self, data: bytes, level: int, scale: Fraction, noise_bits: float) -> CipherVec:
+        k = self._payload_head(data, level)
+        words = np.frombuffer(data, dtype="<u8", count=2 * k * self.n, offset=8).reshape(2, k, self.n)
+        return self._cipher(DevCipher(self._coeffs_to_rows_dev(words), k), level, Fraction(scale), noise_bits)
+
+    def batch_payloads(self, batch: CipherBatch) -> list[bytes]:
+        """cipher_payload_bytes of every item of a batch (one device conversion)."""
+        k = batch.k
+        words = self._rows_to_coeffs(batch.buf[:, :, :k])
+        head = struct.pack("<II", k, self.n)
+        return [head + np.ascontiguousarray(w, dtype="<u8").tobytes() for w in words]
+
+    def batch_from_payloads(self, payloads, level: int, scale: Fraction,
+                            noise_bits: float = float("-inf")) -> CipherBatch:
+        """Inverse of ``batch_payloads``: B payloads at one level -> a (B, 2, k, N) batch."""
+        payloads = list(payloads)
+        k = level + 1
+        words = np.empty((len(payloads), 2, k, self.n), dtype=np.uint64)
+        for i, data in enumerate(payloads):
+            self._payload_head(data, level)
+            words[i] = np.frombuffer(data, dtype="<u8", count=2 * k * self.n, offset=8).reshape(2, k, self.n)
+        return CipherBatch(self._coeffs_to_rows_dev(words), level, Fraction(scale), noise_bits)
+
+    def key_payload_bytes(self, key: KeyMaterial) -> dict[str, bytes]:
+        """Key roles in the reference's array format (ckks.py:456-466): eval-domain
+        Montgomery residues exactly as keygen produced them."""
+        parts: dict[str, bytes] = {}
+        if key.secret is not None:
+            parts["secret"] = ser.pack_array(dev_to_u64(key.secret.s_eval))
+        if key.public is not None:
+            parts["public"] = ser.pack_array(dev_to_u64(key.public.b)) + ser.pack_array(dev_to_u64(key.public.a))
+        if key.evaluation is not None:
+            ev = key.evaluation
+            parts["evaluation"] = ser.pack_array(dev_to_u64(ev.b)) + ser.pack_array(dev_to_u64(ev.a))
+        return parts
+
+    def key_from_payload(self, parts: dict[str, bytes]) -> KeyMaterial:
+        """ckks.py:468-487; the evaluation key is uploaded and Shoup-prepared on the device."""
+        secret = public = evaluation = None
+        if "secret" in parts:
+            s, _ = ser.unpack_array(parts["secret"])
+            secret = DevSecret(u64_to_dev(s, self.dev))
+        if "public" in parts:
+            b, off = ser.unpack_array(parts["public"])
+            a, _ = ser.unpack_array(parts["public"], off)
+            public = DevPublic(b=u64_to_dev(b, self.dev), a=u64_to_dev(a, self.dev))
+        if "evaluation" in parts:
+            b, off = ser.unpack_array(parts["evaluation"])
+            a, _ = ser.unpack_array(parts["evaluation"], off)
+            if b.shape != (self.chain.num_rows - 1, self.chain.num_rows, self.n) or a.shape != b.shape:
+                raise FingerprintMismatch("evaluation key payload does not match parameters")
+            evaluation = self.prepare_switch_key(u64_to_dev(b, self.dev), u64_to_dev(a, self.dev))
+        torch.cuda.synchronize(self.dev)
+        return KeyMaterial(fingerprint=self.fingerprint, backend_name=self.name, secret=secret, public=public,
+                           evaluation=evaluation)
 
     def batch_to_cipher(self, batch: CipherBatch, i: int) -> CipherVec:
         return self._cipher(DevCipher(batch.buf[i], batch.k), batch.level, batch.scale, batch.noise_bits)

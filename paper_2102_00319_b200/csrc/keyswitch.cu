@@ -400,7 +400,11 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
     const int64_t chunk = c->chunk > 0 ? c->chunk : count;
     const int64_t cmax = std::min<int64_t>(chunk, count);
     // ModUp sub-chunk: enough (item, t, j) transforms for ~8 CTA waves, V kept small
-    const int64_t sub = std::max<int64_t>(8, std::min<int64_t>(cmax, (2400 + k * k - 1) / (k * k)));
+    static const int64_t target_ctas = [] {
+        const char *e = getenv("HEB_MODUP_CTAS");
+        return e ? std::max<int64_t>(64, atoll(e)) : (int64_t)2400;
+    }();
+    const int64_t sub = std::max<int64_t>(4, std::min<int64_t>(cmax, (target_ctas + k * k - 1) / (k * k)));
     Scratch sD(st), sA(st), sP(st), sL(st), sV(st);
     CUDA_TRY(sD.get(sizeof(i64) * (size_t)cmax * k * n));
     CUDA_TRY(sA.get(sizeof(u64) * (size_t)cmax * 2 * (k + 1) * n));

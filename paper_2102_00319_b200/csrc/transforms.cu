@@ -9,7 +9,7 @@
 #endif
 template <int LOGN>
 __global__ void __launch_bounds__((KT<LOGN, PLAIN_E>), NTT_MINB_T((KT<LOGN, PLAIN_E>)))
-    k_ntt_fwd(Ctx K, u64 *data, int64_t count, int row0, int64_t bstride) {
+    k_ntt_fwd(Ctx K, u64 *data, int64_t count, int row0, int64_t bstride, int mont) {
     constexpr int E = PLAIN_E;
     extern __shared__ u64 sm[];
     const int r = lbx<LOGN>(), prime = row0 + r;
@@ -17,7 +17,11 @@ __global__ void __launch_bounds__((KT<LOGN, PLAIN_E>), NTT_MINB_T((KT<LOGN, PLAI
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         u64 *row = data + b * bstride + ((int64_t)r << LOGN);
         u64 y[E];
-        fwd_any<LOGN, E>(K, prime, P, sm, [&](int i) { return __ldcg(row + i); }, y);
+        // mont: standard-form coefficients in, Montgomery evaluation rows out (to_mont + NTT)
+        fwd_any<LOGN, E>(K, prime, P, sm, [&](int i) {
+            const u64 v = __ldcg(row + i);
+            return mont ? shoup(v, P.rmod, P.rmod_s, P.p) : v;
+        }, y);
         // all reads of `row` (by both CTAs of a split row) done before in-place writes
         if constexpr (Row<LOGN>::SPLIT) cooperative_groups::this_cluster().sync();
         else __syncthreads();
@@ -27,7 +31,7 @@ __global__ void __launch_bounds__((KT<LOGN, PLAIN_E>), NTT_MINB_T((KT<LOGN, PLAI
 
 template <int LOGN>
 __global__ void __launch_bounds__((KT<LOGN, PLAIN_E>), NTT_MINB_T((KT<LOGN, PLAIN_E>)))
-    k_ntt_inv(Ctx K, u64 *data, int64_t count, int row0, int64_t bstride) {
+    k_ntt_inv(Ctx K, u64 *data, int64_t count, int row0, int64_t bstride, int mont) {
     constexpr int E = PLAIN_E;
     extern __shared__ u64 sm[];
     const int r = lbx<LOGN>(), prime = row0 + r;
@@ -36,22 +40,23 @@ __global__ void __launch_bounds__((KT<LOGN, PLAIN_E>), NTT_MINB_T((KT<LOGN, PLAI
         u64 *row = data + b * bstride + ((int64_t)r << LOGN);
         u64 x[E];
         loadv(row + tpos<LOGN, E>(), x);
-        inv_any<LOGN, E>(K, prime, P, sm, x, [&](int i, u64 v) { row[i] = v; }, false);
+        // mont: Montgomery evaluation rows in, standard-form coefficients out (INTT + from_mont)
+        inv_any<LOGN, E>(K, prime, P, sm, x, [&](int i, u64 v) { row[i] = v; }, mont != 0);
     }
 }
 
 template <int LOGN>
 static int launch_ntt(heb_ctx *c, uint64_t *data, int64_t count, int rows, int row0, int64_t bstride,
-                      cudaStream_t st, bool inverse) {
+                      cudaStream_t st, bool inverse, int mont) {
     constexpr int T = KT<LOGN>;
     constexpr size_t sm = smem_bytes<LOGN>();
     dim3 grid(rows, gdim(count));
     if (inverse) {
         CUDA_TRY(prep_kernel(k_ntt_inv<LOGN>, sm));
-        { PROF("k_ntt_inv", st, 16.0 * c->n * rows * count); CUDA_TRY(launch_rows<LOGN>(k_ntt_inv<LOGN>, dim3(grid), KT<LOGN, PLAIN_E>, sm, st, kctx(c), data, count, row0, bstride)); }
+        { PROF("k_ntt_inv", st, 16.0 * c->n * rows * count); CUDA_TRY(launch_rows<LOGN>(k_ntt_inv<LOGN>, dim3(grid), KT<LOGN, PLAIN_E>, sm, st, kctx(c), data, count, row0, bstride, mont)); }
     } else {
         CUDA_TRY(prep_kernel(k_ntt_fwd<LOGN>, sm));
-        { PROF("k_ntt_fwd", st, 16.0 * c->n * rows * count); CUDA_TRY(launch_rows<LOGN>(k_ntt_fwd<LOGN>, dim3(grid), KT<LOGN, PLAIN_E>, sm, st, kctx(c), data, count, row0, bstride)); }
+        { PROF("k_ntt_fwd", st, 16.0 * c->n * rows * count); CUDA_TRY(launch_rows<LOGN>(k_ntt_fwd<LOGN>, dim3(grid), KT<LOGN, PLAIN_E>, sm, st, kctx(c), data, count, row0, bstride, mont)); }
     }
     LAUNCH_CHECK();
     return HEB_OK;
@@ -61,13 +66,23 @@ extern "C" int heb_ntt_fwd(heb_ctx *c, uint64_t *data, int64_t count, int rows, 
                            void *stream) {
     if (!c || !data || rows < 1 || row0 < 0 || row0 + rows > c->num_rows) return fail(HEB_EINVAL, "heb_ntt_fwd: bad rows");
     if (count <= 0) return HEB_OK;
-    DISPATCH_LOGN(c, launch_ntt, c, data, count, rows, row0, bstride, (cudaStream_t)stream, false);
+    DISPATCH_LOGN(c, launch_ntt, c, data, count, rows, row0, bstride, (cudaStream_t)stream, false, 0);
 }
 extern "C" int heb_ntt_inv(heb_ctx *c, uint64_t *data, int64_t count, int rows, int row0, int64_t bstride,
                            void *stream) {
     if (!c || !data || rows < 1 || row0 < 0 || row0 + rows > c->num_rows) return fail(HEB_EINVAL, "heb_ntt_inv: bad rows");
     if (count <= 0) return HEB_OK;
-    DISPATCH_LOGN(c, launch_ntt, c, data, count, rows, row0, bstride, (cudaStream_t)stream, true);
+    DISPATCH_LOGN(c, launch_ntt, c, data, count, rows, row0, bstride, (cudaStream_t)stream, true, 0);
+}
+extern "C" int heb_coeff_to_eval(heb_ctx *c, uint64_t *data, int64_t count, int rows, int64_t bstride, void *stream) {
+    if (!c || !data || rows < 1 || rows > c->num_rows) return fail(HEB_EINVAL, "heb_coeff_to_eval: bad rows");
+    if (count <= 0) return HEB_OK;
+    DISPATCH_LOGN(c, launch_ntt, c, data, count, rows, 0, bstride, (cudaStream_t)stream, false, 1);
+}
+extern "C" int heb_eval_to_coeff(heb_ctx *c, uint64_t *data, int64_t count, int rows, int64_t bstride, void *stream) {
+    if (!c || !data || rows < 1 || rows > c->num_rows) return fail(HEB_EINVAL, "heb_eval_to_coeff: bad rows");
+    if (count <= 0) return HEB_OK;
+    DISPATCH_LOGN(c, launch_ntt, c, data, count, rows, 0, bstride, (cudaStream_t)stream, true, 1);
 }
 
 // spread_centered + ntt_fwd_rows (ckks.py:120-126): signed coefficient -> (v mod p) * R, NTT

@@ -134,12 +134,24 @@ def small_ring(golden: dict) -> dict:
     # drop + aligned multiply
     a3 = be.drop_to_level(a, 3)
     put("drop_mul", be.mul_ct_ct(a3, b))
+    # serialization: coefficient-form payloads, a full ciphertext envelope, key payloads
+    from hecnn import serialization as ref_ser
+    for name, ct in (("a", a), ("fin", fin), ("a3", a3)):
+        arrays[f"payload_{name}"] = np.frombuffer(be.cipher_payload_bytes(ct), dtype=np.uint8)
+    arrays["record_fin"] = np.frombuffer(ref_ser.cipher_record(be, fin), dtype=np.uint8)
+    arrays["envelope_fin"] = np.frombuffer(ref_ser.wrap(ref_ser.KIND_CIPHER, be, ref_ser.cipher_record(be, fin)),
+                                           dtype=np.uint8)
+    kp = be.key_payload_bytes(keys)
+    key_digests = {role: hashlib.sha256(data).hexdigest() for role, data in kp.items()}
     golden["s128"] = {
         "m": 256, "L": 260, "r": 30, "seed": 42, "extra": 25,
         "square_trace": trace,
         "fin": {"level": fin.level, "scale": frac(fin.scale), "noise": fin.noise_bits},
         "ctpt": {"level": ctpt.level, "scale": frac(ctpt.scale), "noise": ctpt.noise_bits},
         "counters": be.counters.snapshot().__dict__,
+        "key_payload_sha256": key_digests,
+        "payload_meta": {"a": [a.level, frac(a.scale), a.noise_bits], "fin": [fin.level, frac(fin.scale), fin.noise_bits],
+                         "a3": [a3.level, frac(a3.scale), a3.noise_bits]},
     }
 
     # mini CNNs composed from reference API calls
@@ -221,6 +233,7 @@ def baseline_configs(golden: dict) -> None:
         rec["ops"].append({
             "x": ct_digest(x), "y": ct_digest(y), "mul": ct_digest(mul),
             "ctpt": ct_digest(ctpt), "add": ct_digest(add),
+            "mul_payload": hashlib.sha256(be.cipher_payload_bytes(mul)).hexdigest(),
             "mul_dec8": be.decrypt(mul, keys).values[:8].tolist(),
             "mul_scale": frac(mul.scale),
         })

@@ -190,6 +190,7 @@ def test_cfg1_digests_match_reference(golden):
         assert cd(x) == rec["x"] and cd(y) == rec["y"]
         mul = be.mul_ct_ct(x, y)
         assert cd(mul) == rec["mul"]
+        assert hashlib.sha256(be.cipher_payload_bytes(mul)).hexdigest() == rec["mul_payload"]
         assert cd(be.mul_ct_pt(x, be.encode_plain(ys[i], level=x.level))) == rec["ctpt"]
         assert cd(be.add_ct_ct(x, y)) == rec["add"]
         assert list(be.decrypt(mul, keys).values[:8]) == rec["mul_dec8"]
