@@ -106,8 +106,9 @@ static inline Ctx kctx(const heb_ctx *c) {
 // ---------------------------------------------------------------------------------
 // Row geometry.  Rows of N <= 2^14 residues are owned by one CTA; N = 2^15 rows are
 // split over a 2-CTA cluster (blockIdx.x = 2 * logical index + half).  Kernels use
-// lbx() for their logical x index, tpos() for the first of the E positions a thread
-// holds after a forward transform, KT for their block size.
+// lbx() for their logical x index, tpos() for the first of the positions a thread
+// holds after a forward transform (line pairs: tpos + (m & 1) + 2 T (m >> 1), see
+// ntt::lpos; load16/store16 walk that pattern), KT for their block size.
 template <int LOGN>
 struct Row {
 #ifndef SPLIT_MIN_LOGN
@@ -129,9 +130,16 @@ __device__ __forceinline__ int rhalf() {
 }
 template <int LOGN, int E = 16>
 __device__ __forceinline__ int tpos() {
-    return (rhalf<LOGN>() << Row<LOGN>::LL) + (int)threadIdx.x * E;
+    return (rhalf<LOGN>() << Row<LOGN>::LL) + 2 * (int)threadIdx.x;
 }
-
+// HEB_PATH_PROBE (build experiments only): 1 = FP64 engine only, 2 = integer engine only
+#if defined(HEB_PATH_PROBE) && HEB_PATH_PROBE == 1
+#define HEB_FPSEL(x) true
+#elif defined(HEB_PATH_PROBE) && HEB_PATH_PROBE == 2
+#define HEB_FPSEL(x) false
+#else
+#define HEB_FPSEL(x) (x)
+#endif
 // Row-dispatched transforms: rows whose prime is < 2^42 run on the FP64 engine, the
 // others (50/60-bit base and special primes) on the 64-bit integer engine.  Both read
 // u64 residues and return canonical u64 residues, so callers are engine-agnostic.
@@ -139,7 +147,7 @@ template <int LOGN, int E = 16, class Load>
 __device__ __forceinline__ void fwd_any(const Ctx &K, int row, const PrimeInfo &P, u64 *sm, Load load,
                                         u64 (&out)[E]) {
     constexpr int LL = Row<LOGN>::LL;
-    if (P.use_fp) {
+    if (HEB_FPSEL(P.use_fp)) {
         const ntt::FpArith ar(P.pd, P.pinvd);
         double *s = reinterpret_cast<double *>(sm);
         const double *tw = K.twf + ((size_t)row << LOGN);
@@ -158,7 +166,7 @@ __device__ __forceinline__ void inv_any(const Ctx &K, int row, const PrimeInfo &
                                         Store store, bool std_out) {
     constexpr int LL = Row<LOGN>::LL;
     const LastConst &lc = K.last[row];
-    if (P.use_fp) {
+    if (HEB_FPSEL(P.use_fp)) {
         const ntt::FpArith ar(P.pd, P.pinvd);
         double *s = reinterpret_cast<double *>(sm);
         const double *itw = K.itwf + ((size_t)row << LOGN);
@@ -207,20 +215,23 @@ __device__ __forceinline__ const ulonglong2 *itw_row(const Ctx &k, int row) {
     return k.itw + ((size_t)row << LOGN);
 }
 
-// thread's 16 contiguous positions: vectorised load/store
+// a thread's 16 line-pair positions starting at src = row + tpos(): 16-byte accesses,
+// each warp-wide access covers 512 contiguous bytes
+template <int LOGN>
 __device__ __forceinline__ void load16(const u64 *__restrict__ src, u64 (&v)[16]) {
     const ulonglong2 *s = reinterpret_cast<const ulonglong2 *>(src);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        ulonglong2 t = __ldcg(s + i);
+        ulonglong2 t = __ldcg(s + i * KT<LOGN>);
         v[2 * i] = t.x;
         v[2 * i + 1] = t.y;
     }
 }
+template <int LOGN>
 __device__ __forceinline__ void store16(u64 *__restrict__ dst, const u64 (&v)[16]) {
     ulonglong2 *d = reinterpret_cast<ulonglong2 *>(dst);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) __stcg(d + i, make_ulonglong2(v[2 * i], v[2 * i + 1]));
+    for (int i = 0; i < 8; ++i) __stcg(d + i * KT<LOGN>, make_ulonglong2(v[2 * i], v[2 * i + 1]));
 }
 
 // minimum resident CTAs per SM for the NTT kernels: caps registers at 64/thread
@@ -234,22 +245,22 @@ __device__ __forceinline__ void store16(u64 *__restrict__ dst, const u64 (&v)[16
 #define NTT_MINB_T(T) \
     ((65536 / NTT_REGS_PER_THREAD / (T)) > 32 ? 32 : ((65536 / NTT_REGS_PER_THREAD / (T)) < 1 ? 1 : (65536 / NTT_REGS_PER_THREAD / (T))))
 
-// E contiguous positions (E even): 16-byte vector load/store through L2
-template <int E>
+// E line-pair positions (engine with E elements per thread) through L2
+template <int LOGN, int E>
 __device__ __forceinline__ void loadv(const u64 *__restrict__ src, u64 (&v)[E]) {
     const ulonglong2 *s = reinterpret_cast<const ulonglong2 *>(src);
 #pragma unroll
     for (int i = 0; i < E / 2; ++i) {
-        ulonglong2 t = __ldcg(s + i);
+        ulonglong2 t = __ldcg(s + i * KT<LOGN, E>);
         v[2 * i] = t.x;
         v[2 * i + 1] = t.y;
     }
 }
-template <int E>
+template <int LOGN, int E>
 __device__ __forceinline__ void storev(u64 *__restrict__ dst, const u64 (&v)[E]) {
     ulonglong2 *d = reinterpret_cast<ulonglong2 *>(dst);
 #pragma unroll
-    for (int i = 0; i < E / 2; ++i) __stcg(d + i, make_ulonglong2(v[2 * i], v[2 * i + 1]));
+    for (int i = 0; i < E / 2; ++i) __stcg(d + i * KT<LOGN, E>, make_ulonglong2(v[2 * i], v[2 * i + 1]));
 }
 // launch bounds of a row kernel (E = 16 engine)
 #define ROW_BOUNDS(LOGN) __launch_bounds__(KT<LOGN>, NTT_MINB(LOGN))

@@ -16,10 +16,10 @@ __global__ void ROW_BOUNDS(LOGN) k_rescale_head(Ctx K, heb_ct in, const u64 *pt,
     const LastConst lc = K.last[L];
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         u64 x[16];
-        load16(at(in, b, c, L, LOGN) + tpos<LOGN>(), x);
+        load16<LOGN>(at(in, b, c, L, LOGN) + tpos<LOGN>(), x);
         if (pt) {
             u64 y[16];
-            load16(pt + b * pstride + ((int64_t)L << LOGN) + tpos<LOGN>(), y);
+            load16<LOGN>(pt + b * pstride + ((int64_t)L << LOGN) + tpos<LOGN>(), y);
 #pragma unroll
             for (int m = 0; m < 16; ++m) x[m] = mont_mul(x[m], y[m], P.p, P.pinv);
         }
@@ -42,16 +42,16 @@ __global__ void ROW_BOUNDS(LOGN) k_rescale_tail(Ctx K, heb_ct in, const u64 *pt,
         fwd_any<LOGN>(K, i, P, sm,
                            [&](int j) { return signed_mul_const(__ldcg(src + j), C.beta_r.x, C.beta_r.y, P.p); }, y);
         u64 x[16];
-        load16(at(in, b, c, i, LOGN) + tpos<LOGN>(), x);
+        load16<LOGN>(at(in, b, c, i, LOGN) + tpos<LOGN>(), x);
         if (pt) {
             u64 z[16];
-            load16(pt + b * pstride + ((int64_t)i << LOGN) + tpos<LOGN>(), z);
+            load16<LOGN>(pt + b * pstride + ((int64_t)i << LOGN) + tpos<LOGN>(), z);
 #pragma unroll
             for (int m = 0; m < 16; ++m) x[m] = mont_mul(x[m], z[m], P.p, P.pinv);
         }
 #pragma unroll
         for (int m = 0; m < 16; ++m) x[m] = sub_mod(shoup(x[m], C.beta.x, C.beta.y, P.p), y[m], P.p);
-        store16(at(out, b, c, i, LOGN) + tpos<LOGN>(), x);
+        store16<LOGN>(at(out, b, c, i, LOGN) + tpos<LOGN>(), x);
     }
 }
 
@@ -111,7 +111,7 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_head(Ctx K, heb_ct src, int comp, i64 *D, 
     const LastConst lc = K.last[j];
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         u64 x[16];
-        load16(at(src, b, comp, j, LOGN) + tpos<LOGN>(), x);
+        load16<LOGN>(at(src, b, comp, j, LOGN) + tpos<LOGN>(), x);
         i64 *dst = D + (b * k + j) * (1 << LOGN);
         inv_any<LOGN>(K, j, P, sm, x, [&](int i, u64 v) { dst[i] = center(v, P.p); }, true);
     }
@@ -166,7 +166,7 @@ __global__ void ROW_BOUNDS(LOGN)
         const i64 *dj = D + (b * k + j) * n;
         u64 y[16];
         fwd_any<LOGN>(K, gt, P, sm, [&](int i) { return signed_mul_const(__ldcg(dj + i), P.rmod, P.rmod_s, P.p); }, y);
-        store16(V + ((b * (k + 1) + t) * k + j) * n + tpos<LOGN>(), y);
+        store16<LOGN>(V + ((b * (k + 1) + t) * k + j) * n + tpos<LOGN>(), y);
     }
 }
 
@@ -302,10 +302,10 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_down_head(Ctx K, const u64 *acc, heb_ct d,
     const LevelConst C = K.lc[(size_t)(k - 1) * K.num_rows + (k - 1)];
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         u64 x[16];
-        load16(acc + ((b * 2 + c) * (k + 1) + arow) * n + pos, x);
+        load16<LOGN>(acc + ((b * 2 + c) * (k + 1) + arow) * n + pos, x);
         if (which == 1) {
             u64 y[16];
-            load16(at(d, b, c, k - 1, LOGN) + pos, y);
+            load16<LOGN>(at(d, b, c, k - 1, LOGN) + pos, y);
 #pragma unroll
             for (int m = 0; m < 16; ++m) x[m] = add_mod(x[m], shoup(y[m], C.pmod.x, C.pmod.y, P.p), P.p);
             u64 *dst = bL + (b * 2 + c) * n;
@@ -346,14 +346,14 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_down_rescale_tail(Ctx K, const u64 *acc, h
             },
             y);
         u64 x[16], z[16];
-        load16(acc + ((b * 2 + c) * (k + 1) + i) * n + pos, x);
-        load16(at(d, b, c, i, LOGN) + pos, z);
+        load16<LOGN>(acc + ((b * 2 + c) * (k + 1) + i) * n + pos, x);
+        load16<LOGN>(at(d, b, c, i, LOGN) + pos, z);
 #pragma unroll
         for (int m = 0; m < 16; ++m)
             x[m] = sub_mod(add_mod(shoup(x[m], Ci.alpha.x, Ci.alpha.y, Pi.p), shoup(z[m], Ci.beta.x, Ci.beta.y, Pi.p),
                                    Pi.p),
                            y[m], Pi.p);
-        store16(at(out, b, c, i, LOGN) + pos, x);
+        store16<LOGN>(at(out, b, c, i, LOGN) + pos, x);
     }
 }
 
@@ -373,16 +373,16 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_down_tail(Ctx K, const u64 *acc, const i64
         fwd_any<LOGN>(K, i, Pi, sm,
                            [&](int j) { return signed_mul_const(__ldcg(ap + j), Ci.gamma_r.x, Ci.gamma_r.y, Pi.p); }, y);
         u64 x[16];
-        load16(acc + ((b * 2 + c) * (k + 1) + i) * n + pos, x);
+        load16<LOGN>(acc + ((b * 2 + c) * (k + 1) + i) * n + pos, x);
 #pragma unroll
         for (int m = 0; m < 16; ++m) x[m] = sub_mod(shoup(x[m], Ci.gamma.x, Ci.gamma.y, Pi.p), y[m], Pi.p);
         if (c == 0) {
             u64 z[16];
-            load16(at(add0, b, 0, i, LOGN) + pos, z);
+            load16<LOGN>(at(add0, b, 0, i, LOGN) + pos, z);
 #pragma unroll
             for (int m = 0; m < 16; ++m) x[m] = add_mod(x[m], z[m], Pi.p);
         }
-        store16(at(out, b, c, i, LOGN) + pos, x);
+        store16<LOGN>(at(out, b, c, i, LOGN) + pos, x);
     }
 }
 

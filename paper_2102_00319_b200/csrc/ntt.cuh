@@ -32,8 +32,8 @@
 //
 // Interfaces chosen so that callers can fuse prologues/epilogues:
 //   forward: input through a functor load(idx) (coalesced across threads), output
-//            left in registers: thread t holds positions [E t, E t + E) of its row
-//            (of its half for split rows);
+//            left in registers in line-pair order (lpos below) of its row (of its half
+//            for split rows);
 //   inverse: input given in registers in that same layout, output through a functor
 //            store(idx, value) (coalesced).
 // All values handed to the caller are canonical residues.
@@ -45,6 +45,12 @@
 namespace ntt {
 
 HD int pad(int i) { return i + (i >> 4); }
+// Register layout at the engine boundary ("line pairs"): thread t of T holds positions
+// 2t + (m & 1) + 2T (m >> 1), m < E -- every warp-wide 16-byte access covers 512
+// contiguous bytes.  The radix-E groups themselves work on E contiguous positions per
+// thread, so the forward's last group and the inverse's first group transpose through
+// shared memory (conflict-free with the padded index).
+HD int lpos(int t, int m, int T) { return 2 * t + (m & 1) + 2 * T * (m >> 1); }
 
 template <int LOGN, int E = 16>
 struct Shape {
@@ -61,6 +67,11 @@ struct Shape {
 struct IntArith {
     using V = u64;
     using W = ulonglong2;
+#ifndef INT_THROTTLE
+#define INT_THROTTLE 0
+#endif
+    // >0: compiler barrier every THROTTLE butterflies (bounds twiddle-load hoisting)
+    static constexpr int THROTTLE = INT_THROTTLE;
     u64 p, p2;
     HD explicit IntArith(u64 p_) : p(p_), p2(2 * p_) {}
     HD V in(u64 x) const { return x; }
@@ -116,6 +127,7 @@ HD u64 fcanon(double x, double p, double pinv) {
 struct FpArith {
     using V = double;
     using W = double;
+    static constexpr int THROTTLE = 0;
     double p, pinv;
     HD FpArith(double p_, double pinv_) : p(p_), pinv(pinv_) {}
     HD V in(u64 x) const { return u2d(x); }
@@ -177,12 +189,19 @@ HD void fwd_group(const A &ar, typename A::V *sm, const typename A::W *__restric
                 if (m & half) continue;
                 const auto w = __ldg(tw + (c0 << (S0 + q)) + (uhigh << q) + (m >> (RB - q)));
                 ar.fwd(x[m], x[m + half], w);
+                if constexpr (A::THROTTLE > 0) {
+                    if ((m % A::THROTTLE) == A::THROTTLE - 1) asm volatile("" ::: "memory");
+                }
             }
         }
         if constexpr (DST == 1) {
-            static_assert(UPT == 1 && R == E, "register output needs one radix-E unit per thread");
+            static_assert(UPT == 1 && R == E && LB == 0, "register output needs one radix-E unit per thread");
+            // in place (this unit's own positions), then read back in line-pair order
 #pragma unroll
-            for (int m = 0; m < R; ++m) out[m] = ar.out_fwd(x[m]);
+            for (int m = 0; m < R; ++m) sm[pad(base + m)] = x[m];
+            __syncthreads();
+#pragma unroll
+            for (int m = 0; m < R; ++m) out[m] = ar.out_fwd(sm[pad(lpos(tid, m, S::T))]);
         } else {
 #pragma unroll
             for (int m = 0; m < R; ++m) sm[pad(base + (m << LB))] = x[m];
@@ -260,9 +279,13 @@ HD void inv_group(const A &ar, typename A::V *sm, const typename A::W *__restric
         const int base = (uhigh << (LOGN - S0)) | ulow;
         V x[R];
         if constexpr (SRC == 1) {
-            static_assert(UPT == 1 && R == E, "register input needs one radix-E unit per thread");
+            static_assert(UPT == 1 && R == E && LB == 0, "register input needs one radix-E unit per thread");
+            // line-pair order in registers -> this unit's contiguous positions
 #pragma unroll
-            for (int m = 0; m < R; ++m) x[m] = ar.in(in[m]);
+            for (int m = 0; m < R; ++m) sm[pad(lpos(tid, m, S::T))] = ar.in(in[m]);
+            __syncthreads();
+#pragma unroll
+            for (int m = 0; m < R; ++m) x[m] = sm[pad(base + m)];
         } else {
 #pragma unroll
             for (int m = 0; m < R; ++m) x[m] = sm[pad(base + (m << LB))];
@@ -278,6 +301,9 @@ HD void inv_group(const A &ar, typename A::V *sm, const typename A::W *__restric
                 } else {
                     const auto w = __ldg(itw + (c0 << (S0 + q)) + (uhigh << q) + (m >> (RB - q)));
                     ar.inv(x[m], x[m + half], w);
+                    if constexpr (A::THROTTLE > 0) {
+                        if ((m % A::THROTTLE) == A::THROTTLE - 1) asm volatile("" ::: "memory");
+                    }
                 }
             }
         }

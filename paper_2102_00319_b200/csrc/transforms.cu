@@ -25,7 +25,7 @@ __global__ void __launch_bounds__((KT<LOGN, PLAIN_E>), NTT_MINB_T((KT<LOGN, PLAI
         // all reads of `row` (by both CTAs of a split row) done before in-place writes
         if constexpr (Row<LOGN>::SPLIT) cooperative_groups::this_cluster().sync();
         else __syncthreads();
-        storev(row + tpos<LOGN, E>(), y);
+        storev<LOGN, E>(row + tpos<LOGN, E>(), y);
     }
 }
 
@@ -39,7 +39,7 @@ __global__ void __launch_bounds__((KT<LOGN, PLAIN_E>), NTT_MINB_T((KT<LOGN, PLAI
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         u64 *row = data + b * bstride + ((int64_t)r << LOGN);
         u64 x[E];
-        loadv(row + tpos<LOGN, E>(), x);
+        loadv<LOGN, E>(row + tpos<LOGN, E>(), x);
         // mont: Montgomery evaluation rows in, standard-form coefficients out (INTT + from_mont)
         inv_any<LOGN, E>(K, prime, P, sm, x, [&](int i, u64 v) { row[i] = v; }, mont != 0);
     }
@@ -97,7 +97,7 @@ __global__ void ROW_BOUNDS(LOGN) k_spread_ntt(Ctx K, const i64 *coeffs, int64_t 
         u64 y[16];
         fwd_any<LOGN>(K, r, P, sm,
                            [&](int i) { return signed_mul_const(__ldcg(src + i), P.rmod, P.rmod_s, P.p); }, y);
-        store16(out + b * ostride + ((int64_t)r << LOGN) + tpos<LOGN>(), y);
+        store16<LOGN>(out + b * ostride + ((int64_t)r << LOGN) + tpos<LOGN>(), y);
     }
 }
 
@@ -135,15 +135,15 @@ __global__ void ROW_BOUNDS(LOGN) k_encrypt(Ctx K, const i64 *v, const i64 *e0m, 
         u64 V[16], E[16], pk[16], o[16];
         fwd_any<LOGN>(K, r, P, sm, spread(v + b * n), V);
         fwd_any<LOGN>(K, r, P, sm, spread(e0m + b * n), E);
-        load16(pkb + ((size_t)r << LOGN) + pos, pk);
+        load16<LOGN>(pkb + ((size_t)r << LOGN) + pos, pk);
 #pragma unroll
         for (int m = 0; m < 16; ++m) o[m] = add_mod(mont_mul(V[m], pk[m], P.p, P.pinv), E[m], P.p);
-        store16(at(out, b, 0, r, LOGN) + pos, o);
+        store16<LOGN>(at(out, b, 0, r, LOGN) + pos, o);
         fwd_any<LOGN>(K, r, P, sm, spread(e1 + b * n), E);
-        load16(pka + ((size_t)r << LOGN) + pos, pk);
+        load16<LOGN>(pka + ((size_t)r << LOGN) + pos, pk);
 #pragma unroll
         for (int m = 0; m < 16; ++m) o[m] = add_mod(mont_mul(V[m], pk[m], P.p, P.pinv), E[m], P.p);
-        store16(at(out, b, 1, r, LOGN) + pos, o);
+        store16<LOGN>(at(out, b, 1, r, LOGN) + pos, o);
     }
 }
 
@@ -176,9 +176,9 @@ __global__ void ROW_BOUNDS(LOGN) k_decrypt_rows(Ctx K, heb_ct ct, const u64 *s, 
     const int n = 1 << LOGN, pos = tpos<LOGN>();
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         u64 x[16], y[16], z[16];
-        load16(at(ct, b, 1, r, LOGN) + pos, x);
-        load16(s + ((size_t)r << LOGN) + pos, y);
-        load16(at(ct, b, 0, r, LOGN) + pos, z);
+        load16<LOGN>(at(ct, b, 1, r, LOGN) + pos, x);
+        load16<LOGN>(s + ((size_t)r << LOGN) + pos, y);
+        load16<LOGN>(at(ct, b, 0, r, LOGN) + pos, z);
 #pragma unroll
         for (int m = 0; m < 16; ++m) x[m] = add_mod(mont_mul(x[m], y[m], P.p, P.pinv), z[m], P.p);
         u64 *dst = tmp + (b * rows + r) * n;
@@ -244,11 +244,11 @@ __global__ void ROW_BOUNDS(LOGN) k_make_pk(Ctx K, const u64 *s, const u64 *a, co
     fwd_any<LOGN>(K, r, P, sm,
                        [&](int i) { return signed_mul_const(__ldcg(e + i), P.rmod, P.rmod_s, P.p); }, E);
     const size_t off = ((size_t)r << LOGN) + pos;
-    load16(a + off, x);
-    load16(s + off, y);
+    load16<LOGN>(a + off, x);
+    load16<LOGN>(s + off, y);
 #pragma unroll
     for (int m = 0; m < 16; ++m) E[m] = sub_mod(E[m], mont_mul(x[m], y[m], P.p, P.pinv), P.p);
-    store16(pkb + off, E);
+    store16<LOGN>(pkb + off, E);
 }
 
 // kb[j][r] = e_j - a_j,r s_r  (+ (P mod q_j) R * target_j on r == j, applied with mont_mul)
@@ -265,18 +265,18 @@ __global__ void ROW_BOUNDS(LOGN) k_make_swk(Ctx K, const u64 *s, const u64 *targ
     fwd_any<LOGN>(K, r, P, sm,
                        [&](int i) { return signed_mul_const(__ldcg(ej + i), P.rmod, P.rmod_s, P.p); }, E);
     const size_t off = (((size_t)j * R + r) << LOGN) + pos;
-    load16(a + off, x);
-    load16(s + ((size_t)r << LOGN) + pos, y);
+    load16<LOGN>(a + off, x);
+    load16<LOGN>(s + ((size_t)r << LOGN) + pos, y);
 #pragma unroll
     for (int m = 0; m < 16; ++m) E[m] = sub_mod(E[m], mont_mul(x[m], y[m], P.p, P.pinv), P.p);
     if (r == j) {
         // factor = (P mod q_j) * R mod q_j (Montgomery); mont_mul(target, factor) = target * P
         const LevelConst C = K.lc[(size_t)(R - 2) * R + j];  // P mod q_j
-        load16(target + ((size_t)r << LOGN) + pos, x);
+        load16<LOGN>(target + ((size_t)r << LOGN) + pos, x);
 #pragma unroll
         for (int m = 0; m < 16; ++m) E[m] = add_mod(E[m], shoup(x[m], C.pmod.x, C.pmod.y, P.p), P.p);
     }
-    store16(kb + off, E);
+    store16<LOGN>(kb + off, E);
 }
 
 template <int LOGN>

@@ -187,9 +187,14 @@ class TestDevicePayloads:
         for role, data in parts.items():
             assert hashlib.sha256(data).hexdigest() == golden["s128"]["key_payload_sha256"][role], role
         k2 = be.key_from_payload(parts)
-        import torch
-
-        assert torch.equal(k2.evaluation.prep, keys.evaluation.prep)
+        a = _dev_ct(be, s128, golden, "a")
+        want = be.cipher_rows_host(be.mul_ct_ct(a, a))
+        try:
+            be.set_eval_key(k2)
+            got = be.cipher_rows_host(be.mul_ct_ct(a, a))
+        finally:
+            be.set_eval_key(keys)
+        assert all(np.array_equal(x, y) for x, y in zip(got, want))
 
     @pytest.mark.parametrize("log_n", [12, 13, 14, 15])
     def test_round_trip_large_rings(self, log_n):
