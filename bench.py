@@ -22,6 +22,7 @@ not present on the GPU box).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -75,6 +76,13 @@ class Clocks:
         self.device = device
         self.proc = None
         self.path = None
+        self.offset = 0
+
+    def mark(self):
+        """Start of the timed region: only samples written after this count.  The
+        sampler itself is started well before (nvidia-smi start-up perturbs the GPU)."""
+        time.sleep(0.12)
+        self.offset = os.path.getsize(self.path) if self.path else 0
 
     def start(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
@@ -96,7 +104,10 @@ class Clocks:
             self.proc.kill()
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
+        with open(self.path) as fh:
+            fh.seek(self.offset)
+            lines = fh.read().splitlines()
+        for line in lines:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 7:
                 continue
@@ -164,21 +175,30 @@ def run_gpu(args) -> None:
     err = float(np.max(np.abs(dec[:256] - ref)))
     argmax_ok = bool(np.array_equal(np.argmax(dec[:256], 1), np.argmax(ref, 1)))
 
+    clocks = Clocks(local)
+    clocks.start()
     ev.run_many(enc, x, max(args.warmup, args.pipelines), pipelines=args.pipelines, on_output=lambda s, o: gather(o))
     torch.cuda.synchronize()
 
     # ---- device-resident timed region -------------------------------------------------
-    clocks = Clocks(local)
-    clocks.start()
+    clocks.mark()
+    gc.disable()  # no collector pauses while the host enqueues the timed steps
     barrier()
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    marks = [] if os.environ.get("HEB_TIMELINE") else None
+    h0 = time.perf_counter()
     t0.record(stream)
-    ev.run_many(enc, x, args.steps, pipelines=args.pipelines, on_output=lambda s, o: gather(o))
+    ev.run_many(enc, x, args.steps, pipelines=args.pipelines, on_output=lambda s, o: gather(o), marks=marks)
     t1.record(stream)
     torch.cuda.synchronize()
     barrier()
+    gc.enable()
+    if marks:
+        for s, (p, b, e, h) in enumerate(marks):
+            print(f"timeline step {s} pipe {p}: start {t0.elapsed_time(b):8.2f} end {t0.elapsed_time(e):8.2f}"
+                  f"  host enqueued {(h - h0) * 1e3:8.2f}", file=sys.stderr)
     clk = clocks.stop()
     ms = t0.elapsed_time(t1)
     ms_t = torch.tensor([ms], device="cuda")
@@ -223,11 +243,13 @@ def run_gpu(args) -> None:
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    gc.disable()
     e0.record(stream)
     e2e_run(args.steps)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
+    gc.enable()
     e2e_ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)

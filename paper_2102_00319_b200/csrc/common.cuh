@@ -6,7 +6,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/heb200.h"
@@ -66,6 +69,16 @@ struct LastConst {  // final inverse-stage factors (Shoup pairs; FP64 engine: (w
     double fu_plain, fv_plain, fu_std, fv_std;
 };
 
+struct StreamArena {
+    struct Block {
+        char *base;
+        size_t cap;
+    };
+    std::recursive_mutex mu;
+    std::vector<Block> blocks;
+    size_t blk = 0, off = 0;  // bump position
+};
+
 struct heb_ctx {
     int device = 0, log_n = 0, n = 0, num_rows = 0, chunk = 1024;
     std::vector<u64> primes;
@@ -75,18 +88,63 @@ struct heb_ctx {
     LevelConst *d_lc = nullptr;
     LastConst *d_last = nullptr;
     int flush = 64;  // lazy 128-bit accumulation: products summed before a reduction
-};
-
-// scoped stream-ordered scratch
-struct Scratch {
-    void *p = nullptr;
-    cudaStream_t s;
-    explicit Scratch(cudaStream_t st) : s(st) {}
-    cudaError_t get(size_t bytes) { return cudaMallocAsync(&p, bytes ? bytes : 8, s); }
-    ~Scratch() {
-        if (p) cudaFreeAsync(p, s);
+    std::mutex arena_mu;
+    std::unordered_map<cudaStream_t, std::unique_ptr<StreamArena>> arenas;
+    StreamArena *arena(cudaStream_t st) {
+        std::lock_guard<std::mutex> g(arena_mu);
+        auto &a = arenas[st];
+        if (!a) a.reset(new StreamArena());
+        return a.get();
     }
 };
+
+// Per-stream scratch arena.  Kernel intermediates (key-switch digits, ModUp outputs,
+// ...) come from a chain of device blocks owned by the context and keyed by stream;
+// Scratch objects take and return space in LIFO order, so a call's scratch is reused by
+// the next call on the same stream (stream order makes that safe).  Blocks are only
+// ever added (cudaMalloc, during the first calls of a shape) -- steady-state calls and
+// CUDA-graph replays touch no allocator, and concurrent streams never share memory.
+// One host thread at a time may issue calls on a stream (a recursive lock per stream
+// arena covers the lifetime of a call's Scratch objects).
+struct Scratch {
+    void *p = nullptr;
+    StreamArena *a;
+    size_t blk0, off0;
+    std::unique_lock<std::recursive_mutex> lock;
+    Scratch(heb_ctx *c, cudaStream_t st);
+    cudaError_t get(size_t bytes) {
+        bytes = (bytes + 255) & ~(size_t)255;
+        if (!bytes) bytes = 256;
+        while (a->blk < a->blocks.size()) {
+            auto &b = a->blocks[a->blk];
+            if (a->off + bytes <= b.cap) {
+                p = b.base + a->off;
+                a->off += bytes;
+                return cudaSuccess;
+            }
+            ++a->blk;
+            a->off = 0;
+        }
+        size_t cap = a->blocks.empty() ? (size_t)64 << 20 : a->blocks.back().cap * 2;
+        if (cap < bytes) cap = bytes;
+        void *q = nullptr;
+        cudaError_t e = cudaMalloc(&q, cap);
+        if (e != cudaSuccess) return e;
+        a->blocks.push_back({(char *)q, cap});
+        a->blk = a->blocks.size() - 1;
+        p = q;
+        a->off = bytes;
+        return cudaSuccess;
+    }
+    ~Scratch() {
+        a->blk = blk0;
+        a->off = off0;
+    }
+};
+inline Scratch::Scratch(heb_ctx *c, cudaStream_t st) : a(c->arena(st)), lock(a->mu) {
+    blk0 = a->blk;
+    off0 = a->off;
+}
 
 // =============================================================================
 // device helpers

@@ -186,13 +186,16 @@ extern "C" int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows
         heb_ctx_destroy(c);
         return fail(HEB_ECUDA, "context upload failed: %s", cudaGetErrorString(e));
     }
-    // Keep freed stream-ordered scratch in the pool: without a release threshold the
-    // key-switch intermediates (hundreds of MB per layer) are unmapped and remapped
-    // around every synchronisation.
+    // heb_alloc memory is stream-ordered: keep freed blocks in the pool (no unmapping
+    // around every synchronisation).  Never let the pool satisfy an allocation on one
+    // stream with memory freed on another by inserting a wait on that stream: with
+    // concurrent inference pipelines such hidden dependencies serialise the pipelines.
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
         uint64_t keep = ~0ull;
+        int no = 0;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
     }
     *out = c;
     return HEB_OK;
@@ -207,6 +210,11 @@ extern "C" int heb_ctx_destroy(heb_ctx *c) {
     cudaFree(c->d_itwf);
     cudaFree(c->d_lc);
     cudaFree(c->d_last);
+    if (!c->arenas.empty()) {
+        cudaDeviceSynchronize();  // scratch may still be in use by queued work
+        for (auto &kv : c->arenas)
+            for (auto &b : kv.second->blocks) cudaFree(b.base);
+    }
     delete c;
     return HEB_OK;
 }

@@ -63,7 +63,7 @@ static int launch_rescale(heb_ctx *c, heb_ct in, const u64 *pt, int64_t pstride,
     CUDA_TRY(prep_kernel(k_rescale_head<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_rescale_tail<LOGN>, sm));
     const int64_t chunk = c->chunk > 0 ? c->chunk * 4 : count;
-    Scratch V(st);
+    Scratch V(c, st);
     CUDA_TRY(V.get(sizeof(i64) * (size_t)std::min<int64_t>(count, chunk) * comps * c->n));
     for (int64_t b0 = 0; b0 < count; b0 += chunk) {
         const int64_t cnt = std::min<int64_t>(chunk, count - b0);
@@ -171,78 +171,87 @@ __global__ void ROW_BOUNDS(LOGN)
 }
 
 // acc[item][c][t][x] = sum_j v_j[x] * key_c[j][gt][x]  (Shoup with the prepared key)
-__global__ void k_ks_modup_mac(Ctx K, heb_ct src, int comp, const u64 *V, const ulonglong2 *key, int k, u64 *acc,
+// Each thread owns two adjacent positions (16-byte accesses) and issues the loads of
+// MJ digits before using them, so every thread keeps MJ HBM reads in flight -- the
+// kernel is a stream over V and needs that memory-level parallelism.
+#ifndef MAC_MJ
+#define MAC_MJ 4
+#endif
+#ifndef MAC_MINB
+#define MAC_MINB 4
+#endif
+template <bool FP>
+__global__ void __launch_bounds__(256, MAC_MINB) k_ks_modup_mac(Ctx K, heb_ct src, int comp, const u64 *V, const ulonglong2 *key, int k, u64 *acc,
                                int64_t count, int logn) {
     const int n = 1 << logn;
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int x = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
     const int t = blockIdx.y;
     const int gt = t < k ? t : K.num_rows - 1;
     const PrimeInfo P = K.pi[gt];
     const u64 p2 = 2 * P.p;
-    if (x >= n) return;
-    if (P.use_fp) {
-        // FP64 rows: the prepared key holds w as doubles (b part then a part), products
-        // are exact FP64 modular products, sums stay exact below 2^47.  Each thread
-        // serves MI items so every key word read from L2 is used MI times.
-        constexpr int MI = 1;
-        for (int64_t b0 = (int64_t)blockIdx.z * MI; b0 < count; b0 += (int64_t)gridDim.z * MI) {
-            const int nb = (int)(count - b0 < MI ? count - b0 : MI);
-            double s0[MI], s1[MI];
+    if (x >= n || P.use_fp != FP) return;  // launched once per engine; rows of the other engine exit
+    for (int64_t b = blockIdx.z; b < count; b += gridDim.z) {
+        const u64 *vrow = V + ((b * (k + 1) + t) * k) * n + x;
+        const u64 *own = at(src, b, comp, t < k ? t : 0, logn) + x;
+        u64 *o0 = acc + ((b * 2 + 0) * (k + 1) + t) * n + x;
+        u64 *o1 = acc + ((b * 2 + 1) * (k + 1) + t) * n + x;
+        if constexpr (FP) {
+            // FP64 rows: the prepared key holds w as doubles (b part then a part);
+            // exact FP64 modular products, sums stay exact below 2^47
+            double s0x = 0.0, s0y = 0.0, s1x = 0.0, s1y = 0.0;
+            for (int j0 = 0; j0 < k; j0 += MAC_MJ) {
+                ulonglong2 v[MAC_MJ];
+                double2 kb[MAC_MJ], ka[MAC_MJ];
 #pragma unroll
-            for (int g = 0; g < MI; ++g) s0[g] = s1[g] = 0.0;
-            for (int j = 0; j < k; ++j) {
-                const double *kd = reinterpret_cast<const double *>(key + (((size_t)j * K.num_rows + gt) * 2) * n);
-                const double kb = __ldg(kd + x), ka = __ldg(kd + n + x);
+                for (int u = 0; u < MAC_MJ; ++u) {
+                    const int j = j0 + u;
+                    if (j < k) {
+                        const u64 *vp = (j == t) ? own : vrow + (size_t)j * n;
+                        v[u] = __ldcg(reinterpret_cast<const ulonglong2 *>(vp));
+                        const double *kd = reinterpret_cast<const double *>(key + (((size_t)j * K.num_rows + gt) * 2) * n);
+                        kb[u] = __ldg(reinterpret_cast<const double2 *>(kd + x));
+                        ka[u] = __ldg(reinterpret_cast<const double2 *>(kd + n + x));
+                    }
+                }
 #pragma unroll
-                for (int g = 0; g < MI; ++g) {
-                    if (g < nb) {
-                        const int64_t b = b0 + g;
-                        const u64 v = (j == t) ? __ldcg(at(src, b, comp, j, logn) + x)
-                                               : __ldcg(V + ((b * (k + 1) + t) * k + j) * n + x);
-                        const double vd = ntt::u2d(v);
-                        s0[g] += ntt::fmul(vd, kb, P.pd, P.pinvd);
-                        s1[g] += ntt::fmul(vd, ka, P.pd, P.pinvd);
+                for (int u = 0; u < MAC_MJ; ++u) {
+                    if (j0 + u < k) {
+                        const double vx = ntt::u2d(v[u].x), vy = ntt::u2d(v[u].y);
+                        s0x += ntt::fmul(vx, kb[u].x, P.pd, P.pinvd);
+                        s0y += ntt::fmul(vy, kb[u].y, P.pd, P.pinvd);
+                        s1x += ntt::fmul(vx, ka[u].x, P.pd, P.pinvd);
+                        s1y += ntt::fmul(vy, ka[u].y, P.pd, P.pinvd);
                     }
                 }
             }
+            __stcg(reinterpret_cast<ulonglong2 *>(o0),
+                   make_ulonglong2(ntt::fcanon(s0x, P.pd, P.pinvd), ntt::fcanon(s0y, P.pd, P.pinvd)));
+            __stcg(reinterpret_cast<ulonglong2 *>(o1),
+                   make_ulonglong2(ntt::fcanon(s1x, P.pd, P.pinvd), ntt::fcanon(s1y, P.pd, P.pinvd)));
+        } else {
+        u64 s0x = 0, s0y = 0, s1x = 0, s1y = 0;
+        for (int j0 = 0; j0 < k; j0 += MAC_MJ) {
+            ulonglong2 v[MAC_MJ];
 #pragma unroll
-            for (int g = 0; g < MI; ++g) {
-                if (g < nb) {
-                    const int64_t b = b0 + g;
-                    __stcg(acc + ((b * 2 + 0) * (k + 1) + t) * n + x, ntt::fcanon(s0[g], P.pd, P.pinvd));
-                    __stcg(acc + ((b * 2 + 1) * (k + 1) + t) * n + x, ntt::fcanon(s1[g], P.pd, P.pinvd));
+            for (int u = 0; u < MAC_MJ; ++u) {
+                const int j = j0 + u;
+                if (j < k) v[u] = __ldcg(reinterpret_cast<const ulonglong2 *>((j == t) ? own : vrow + (size_t)j * n));
+            }
+#pragma unroll
+            for (int u = 0; u < MAC_MJ; ++u) {
+                const int j = j0 + u;
+                if (j < k) {
+                    const ulonglong2 *kp = key + (((size_t)j * K.num_rows + gt) * 2) * n + x;
+                    const ulonglong2 bx = __ldg(kp), by = __ldg(kp + 1), ax = __ldg(kp + n), ay = __ldg(kp + n + 1);
+                    s0x = csub(s0x + shoup_lazy(v[u].x, bx.x, bx.y, P.p), p2);
+                    s0y = csub(s0y + shoup_lazy(v[u].y, by.x, by.y, P.p), p2);
+                    s1x = csub(s1x + shoup_lazy(v[u].x, ax.x, ax.y, P.p), p2);
+                    s1y = csub(s1y + shoup_lazy(v[u].y, ay.x, ay.y, P.p), p2);
                 }
             }
         }
-        return;
-    }
-    constexpr int MI = 1;
-    for (int64_t b0 = (int64_t)blockIdx.z * MI; b0 < count; b0 += (int64_t)gridDim.z * MI) {
-        const int nb = (int)(count - b0 < MI ? count - b0 : MI);
-        u64 s0[MI], s1[MI];
-#pragma unroll
-        for (int g = 0; g < MI; ++g) s0[g] = s1[g] = 0;
-        for (int j = 0; j < k; ++j) {
-            const ulonglong2 *kb = key + (((size_t)j * K.num_rows + gt) * 2) * n + x;
-            const ulonglong2 wb = __ldg(kb), wa = __ldg(kb + n);
-#pragma unroll
-            for (int g = 0; g < MI; ++g) {
-                if (g < nb) {
-                    const int64_t b = b0 + g;
-                    const u64 v = (j == t) ? __ldcg(at(src, b, comp, j, logn) + x)
-                                           : __ldcg(V + ((b * (k + 1) + t) * k + j) * n + x);
-                    s0[g] = csub(s0[g] + shoup_lazy(v, wb.x, wb.y, P.p), p2);
-                    s1[g] = csub(s1[g] + shoup_lazy(v, wa.x, wa.y, P.p), p2);
-                }
-            }
-        }
-#pragma unroll
-        for (int g = 0; g < MI; ++g) {
-            if (g < nb) {
-                const int64_t b = b0 + g;
-                __stcg(acc + ((b * 2 + 0) * (k + 1) + t) * n + x, csub(s0[g], P.p));
-                __stcg(acc + ((b * 2 + 1) * (k + 1) + t) * n + x, csub(s1[g], P.p));
-            }
+        __stcg(reinterpret_cast<ulonglong2 *>(o0), make_ulonglong2(csub(s0x, P.p), csub(s0y, P.p)));
+        __stcg(reinterpret_cast<ulonglong2 *>(o1), make_ulonglong2(csub(s1x, P.p), csub(s1y, P.p)));
         }
     }
 }
@@ -405,7 +414,7 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
         return e ? std::max<int64_t>(64, atoll(e)) : (int64_t)2400;
     }();
     const int64_t sub = std::max<int64_t>(4, std::min<int64_t>(cmax, (target_ctas + k * k - 1) / (k * k)));
-    Scratch sD(st), sA(st), sP(st), sL(st), sV(st);
+    Scratch sD(c, st), sA(c, st), sP(c, st), sL(c, st), sV(c, st);
     CUDA_TRY(sD.get(sizeof(i64) * (size_t)cmax * k * n));
     CUDA_TRY(sA.get(sizeof(u64) * (size_t)cmax * 2 * (k + 1) * n));
     CUDA_TRY(sP.get(sizeof(i64) * (size_t)cmax * 2 * n));
@@ -434,8 +443,9 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
             LAUNCH_CHECK();
             {
                 PROF("k_ks_modup_mac", st, 8.0 * n * (sc * k * (k + 1) + 4.0 * k * (k + 1) + 2.0 * sc * (k + 1)));
-                k_ks_modup_mac<<<dim3((n + 255) / 256, k + 1, gdim(sc)), 256, 0, st>>>(K, ss, comp, (const u64 *)sV.p,
-                                                                                        key, k, Ap, sc, LOGN);
+                const dim3 mg((n / 2 + 255) / 256, k + 1, gdim(sc));
+                k_ks_modup_mac<true><<<mg, 256, 0, st>>>(K, ss, comp, (const u64 *)sV.p, key, k, Ap, sc, LOGN);
+                k_ks_modup_mac<false><<<mg, 256, 0, st>>>(K, ss, comp, (const u64 *)sV.p, key, k, Ap, sc, LOGN);
             }
             LAUNCH_CHECK();
         }
@@ -477,7 +487,7 @@ extern "C" int heb_rotate(heb_ctx *c, heb_ct ct, const uint64_t *gk, heb_ct out,
     cudaStream_t st = (cudaStream_t)stream;
     const int k = level + 1;
     // sigma_g of both components into a compact scratch batch
-    Scratch rot(st);
+    Scratch rot(c, st);
     CUDA_TRY(rot.get(sizeof(u64) * (size_t)count * 2 * k * c->n));
     heb_ct r{(u64 *)rot.p, (int64_t)2 * k * c->n, (int64_t)k * c->n};
     const int64_t lines = count * 2 * k;

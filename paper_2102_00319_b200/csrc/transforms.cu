@@ -213,7 +213,7 @@ static int launch_decrypt(heb_ctx *c, heb_ct ct, const u64 *s, i64 *coeffs, i64 
     constexpr size_t sm = smem_bytes<LOGN>();
     CUDA_TRY(prep_kernel(k_decrypt_rows<LOGN>, sm));
     const int rows = k >= 2 ? 2 : 1;
-    Scratch tmp(st);
+    Scratch tmp(c, st);
     CUDA_TRY(tmp.get(sizeof(u64) * (size_t)count * rows * c->n));
     CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(i64) * count, st));
     { PROF("k_decrypt_rows", st, 8.0 * c->n * (3.0 * count * rows + rows)); CUDA_TRY(launch_rows<LOGN>(k_decrypt_rows<LOGN>, dim3(dim3(rows, gdim(count))), KT<LOGN>, sm, st, kctx(c), ct, s, (u64 *)tmp.p, rows,

@@ -22,6 +22,8 @@ laid out channel-major: item = c*(m*n) + i*n + j.
 
 from __future__ import annotations
 
+import time
+
 import math
 from dataclasses import dataclass
 from fractions import Fraction
@@ -98,6 +100,9 @@ class LayerEvaluator:
         self._idx_cache: dict = {}
         self._unique: dict = {}
         self._streams: dict = {}
+        self._graphs: dict = {}
+        self._pt_cache: dict = {}
+        self._inbufs: dict = {}
 
     # -- primitives -------------------------------------------------------------------
     def _idx(self, key, builder) -> torch.Tensor:
@@ -240,7 +245,11 @@ class LayerEvaluator:
         return y, (F, om, on)
 
     def poly_act(self, y: CipherBatch, act: PolyAct) -> CipherBatch:
-        pt_quad, pt_lin, pt_const = act_plaintexts(self.be, act, y.level, y.scale)
+        key = ("act", act.folded(), y.level, y.scale)
+        pts = self._pt_cache.get(key)
+        if pts is None:  # encoded once per (activation, level, scale); constant plaintexts
+            pts = self._pt_cache[key] = act_plaintexts(self.be, act, y.level, y.scale)
+        pt_quad, pt_lin, pt_const = pts
         c0, c1, c2 = act.folded()
         t = self.square(y)
         quad = self.mul_plain(t, pt_quad, abs(c2))
@@ -313,8 +322,42 @@ class LayerEvaluator:
             pool.append(torch.cuda.Stream(self.be.dev))
         return pool[:count]
 
+    def captured(self, enc: EncryptedNetworkBatch, x: CipherBatch, pipeline: int):
+        """(graph, output, counter delta) -- one inference of ``x`` captured as a CUDA graph.
+
+        The graph replays every launch of ``run`` (and the stream-ordered scratch
+        allocations, as graph memory nodes) with one host call; each pipeline owns its
+        graph and private memory pool, so replays of different pipelines may overlap.
+        The output batch is overwritten by the next replay of the same graph."""
+        key = (id(enc), x.buf.data_ptr(), tuple(x.buf.shape), x.level, pipeline)
+        hit = self._graphs.get(key)
+        if hit is None:
+            st = self._pipeline_streams("compute", pipeline + 1)[pipeline]
+            st.wait_stream(torch.cuda.current_stream(self.be.dev))
+            start = self.be.counters.snapshot().__dict__
+            with torch.cuda.stream(st):
+                self.run(enc, x)  # builds index caches / kernel attributes outside the capture
+            st.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            before = self.be.counters.snapshot().__dict__
+            with torch.cuda.graph(graph, pool=torch.cuda.graph_pool_handle(), stream=st,
+                                  capture_error_mode="thread_local"):
+                out = self.run(enc, x)
+            after = self.be.counters.snapshot().__dict__
+            delta = {f: after[f] - before[f] for f in after}
+            # warm-up and capture are not user-visible evaluations: take their tallies back
+            self.be.counters.bump(**{f: start[f] - after[f] for f in after})
+            hit = self._graphs[key] = (graph, out, delta, enc, x.buf)  # keep the captured buffers alive
+        return hit[:3]
+
+    def _replay(self, runner) -> CipherBatch:
+        graph, out, delta = runner
+        graph.replay()
+        self.be.counters.bump(**delta)  # the op tallies a host-issued run would have made
+        return out
+
     def run_stream(self, enc: EncryptedNetworkBatch, host_inputs, level: int, scale: Fraction, noise: float,
-                   host_outputs, on_output=None, pipelines: int = 2) -> None:
+                   host_outputs, on_output=None, pipelines: int = 2, graphs: bool = True) -> None:
         """Evaluate a sequence of pinned host input batches ((B, 2, K, N) int64 tensors).
 
         Batches are dealt round-robin to ``pipelines`` independent pipelines, each with
@@ -322,15 +365,24 @@ class LayerEvaluator:
         copy of one pipeline's next batch overlaps the other pipelines' evaluation, and
         the pipelines' kernels fill each other's tails on the SMs.  The logits of batch
         s are copied back into ``host_outputs[s]`` (pinned, (out, 2, k, N)).  On return
-        the caller's current stream is ordered after all the work.
+        the caller's current stream is ordered after all the work.  ``graphs``: replay
+        one captured CUDA graph per pipeline instead of re-issuing every launch.
         """
         caller = torch.cuda.current_stream(self.be.dev)
         P = max(1, pipelines)
         comp = self._pipeline_streams("compute", P)
         copy = self._pipeline_streams("copy", P)
+        shape = tuple(host_inputs[0].shape)
+        bufs = []
+        for p in range(P):  # persistent per-pipeline device inputs (graph-captured addresses)
+            b = self._inbufs.get((shape, p))
+            if b is None:
+                b = self._inbufs[(shape, p)] = torch.empty(shape, dtype=host_inputs[0].dtype, device=self.be.dev)
+            bufs.append(b)
+        runners = [self.captured(enc, CipherBatch(bufs[p], level, scale, noise), p) if graphs else None
+                   for p in range(P)]
         for st in comp + copy:
             st.wait_stream(caller)
-        bufs = [torch.empty_like(host_inputs[0], device=self.be.dev) for _ in range(P)]
         copied = [torch.cuda.Event() for _ in range(P)]
         consumed = [torch.cuda.Event() for _ in range(P)]
         for s in range(len(host_inputs)):
@@ -342,7 +394,10 @@ class LayerEvaluator:
                 copied[p].record(copy[p])
             with torch.cuda.stream(comp[p]):
                 comp[p].wait_event(copied[p])
-                out = self.run(enc, CipherBatch(bufs[p], level, scale, noise))
+                if graphs:
+                    out = self._replay(runners[p])
+                else:
+                    out = self.run(enc, CipherBatch(bufs[p], level, scale, noise))
                 consumed[p].record(comp[p])
                 host_outputs[s].copy_(out.buf[:, :, : out.k], non_blocking=True)
                 if on_output is not None:
@@ -351,18 +406,31 @@ class LayerEvaluator:
             caller.wait_stream(st)
 
     def run_many(self, enc: EncryptedNetworkBatch, x: CipherBatch, steps: int, pipelines: int = 2,
-                 on_output=None) -> None:
-        """Evaluate ``steps`` device-resident batches over ``pipelines`` concurrent streams."""
+                 on_output=None, marks: list | None = None, graphs: bool = True) -> None:
+        """Evaluate ``steps`` device-resident batches over ``pipelines`` concurrent streams
+        (``graphs``: one captured CUDA graph per pipeline, see ``captured``).
+        ``marks`` (diagnostics): receives (pipeline, start event, end event, host time) per step."""
         caller = torch.cuda.current_stream(self.be.dev)
         P = max(1, pipelines)
         comp = self._pipeline_streams("compute", P)
+        runners = [self.captured(enc, x, p) for p in range(P)] if graphs else None
         for st in comp:
             st.wait_stream(caller)
         for s in range(steps):
-            with torch.cuda.stream(comp[s % P]):
-                out = self.run(enc, x)
+            p = s % P
+            with torch.cuda.stream(comp[p]):
+                if marks is not None:
+                    b, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    b.record()
+                if graphs:
+                    out = self._replay(runners[p])
+                else:
+                    out = self.run(enc, x)
                 if on_output is not None:
                     on_output(s, out)
+                if marks is not None:
+                    e.record()
+                    marks.append((p, b, e, time.perf_counter()))
         for st in comp:
             caller.wait_stream(st)
 

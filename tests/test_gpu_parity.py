@@ -274,3 +274,38 @@ def test_ring_sweep_ops_match_oracle(m):
     same(dev.rotate(dx, 1), ora.rotate(ox, 1), "rotate")
     same(dev.mul_ct_ct(dm, dm), ora.mul_ct_ct(om, om), "second level")
     assert np.max(np.abs(dev.decrypt(dm, dk).values - x * y)) < 1e-4
+
+
+@pytest.mark.parametrize("pipelines", [1, 3])
+def test_graph_pipelines_match_direct_run(golden, dev_s128, pipelines):
+    """run_many / run_stream replay one captured CUDA graph per pipeline; every step's
+    logits must equal the host-issued run (and the reference digests), and the op
+    counters must advance as if each step had been issued op by op."""
+    import torch
+
+    from nets import mini_networks
+    from paper_2102_00319_b200 import layers
+
+    be, keys = dev_s128
+    net = mini_networks()["mini3"]
+    imgs = np.random.default_rng(13).uniform(0, 1, (be.slots, 12, 12))[:, : net.input_dims[0], : net.input_dims[1]]
+    enc = layers.encrypt_network(be, net, keys)
+    x = layers.encrypt_images(be, imgs, keys)
+    ev = layers.LayerEvaluator(be)
+    be.counters.reset()
+    want = ev.run(enc, x)
+    per_run = be.counters.snapshot().__dict__
+    want_rows = want.buf.clone()
+    seen = []
+    ev.run_many(enc, x, 5, pipelines=pipelines, on_output=lambda s, o: seen.append(o.buf.clone()))
+    torch.cuda.synchronize()
+    assert len(seen) == 5 and all(torch.equal(t, want_rows) for t in seen)
+    digests = [digest(np.concatenate(be.cipher_rows_host(be.batch_to_cipher(want, i)))) for i in range(want.count)]
+    assert digests == golden["minis"]["mini3"]["logit_digests"]
+    host_in = [x.buf.cpu().pin_memory() for _ in range(4)]
+    host_out = [torch.empty((want.count, 2, want.k, be.n), dtype=torch.int64).pin_memory() for _ in range(4)]
+    be.counters.reset()
+    ev.run_stream(enc, host_in, x.level, x.scale, x.noise_bits, host_out, pipelines=pipelines)
+    torch.cuda.synchronize()
+    assert all(torch.equal(h, want_rows[:, :, : want.k].cpu()) for h in host_out)
+    assert be.counters.snapshot().__dict__ == {f: 4 * v for f, v in per_run.items()}
