@@ -175,10 +175,10 @@ __global__ void ROW_BOUNDS(LOGN)
 // MJ digits before using them, so every thread keeps MJ HBM reads in flight -- the
 // kernel is a stream over V and needs that memory-level parallelism.
 #ifndef MAC_MJ
-#define MAC_MJ 4
+#define MAC_MJ 2
 #endif
 #ifndef MAC_MINB
-#define MAC_MINB 4
+#define MAC_MINB 6
 #endif
 template <bool FP>
 __global__ void __launch_bounds__(256, MAC_MINB) k_ks_modup_mac(Ctx K, heb_ct src, int comp, const u64 *V, const ulonglong2 *key, int k, u64 *acc,
