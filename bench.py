@@ -227,16 +227,21 @@ def run_gpu(args) -> None:
 
     # ---- end-to-end: host buffers through the public API -------------------------------
     # Every step copies its input ciphertexts from pinned host memory and its logits
-    # back; LayerEvaluator.run_stream overlaps the copy of batch s+1 with batch s.
-    x_hosts = [torch.empty(x.buf.shape, dtype=x.buf.dtype, pin_memory=True) for _ in range(2)]
+    # back; LayerEvaluator.run_stream overlaps the copy of batch s+1 with batch s.  The
+    # client hands the grid over in the bit-packed wire format (residues at the bit
+    # length of their prime, csrc/packing.cu), unpacked on the device inside the step.
+    x_packed = be.pack_batch(x)
+    x_hosts = [torch.empty(x_packed.shape, dtype=x_packed.dtype, pin_memory=True) for _ in range(2)]
     for h in x_hosts:
-        h.copy_(x.buf)
+        h.copy_(x_packed)
+    del x_packed
     logits_hosts = [torch.empty((out.count, 2, out.k, be.n), dtype=torch.int64, pin_memory=True)
                     for _ in range(args.steps)]
 
     def e2e_run(nsteps):
         ev.run_stream(enc, [x_hosts[s % 2] for s in range(nsteps)], x.level, x.scale, x.noise_bits,
-                      logits_hosts[:nsteps], on_output=lambda s, o: gather(o), pipelines=args.pipelines)
+                      logits_hosts[:nsteps], on_output=lambda s, o: gather(o), pipelines=args.pipelines,
+                      unpacked_shape=tuple(x.buf.shape))
 
     e2e_run(min(args.steps, max(2 * args.pipelines, args.warmup)))
     torch.cuda.synchronize()
@@ -324,7 +329,8 @@ def run_gpu(args) -> None:
             "e2e": {
                 "value": round(e2e_value, 3),
                 "unit": UNIT,
-                "h2d_bytes_per_step": int(x.buf.numel() * 8),
+                "h2d_bytes_per_step": int(x_hosts[0].numel() * 8),
+                "wire_format": "bit-packed residues (heb_pack_rows), unpacked on the device in the step",
                 "d2h_bytes_per_step": int(out.count * 2 * out.k * be.n * 8),
             },
             "gpu_launches": int(launches),

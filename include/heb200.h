@@ -157,6 +157,16 @@ int heb_sum_gather(heb_ctx *ctx, heb_ct a, const int32_t *idx, int terms, heb_ct
 int heb_gather(heb_ctx *ctx, heb_ct a, const int32_t *idx, heb_ct out, int64_t n_out, int comps, int k,
                void *stream);
 
+/* --- transport (host <-> device wire format) --------------------------------------- */
+/* Residue rows bit-packed at bitlen(p_r) bits per residue: a block of rows 0..rows-1
+ * takes heb_packed_words(rows) words (row r: ceil(N*bitlen(p_r)/64) words, in order);
+ * blocks are contiguous.  No reference counterpart (its payloads are u64 words). */
+int64_t heb_packed_words(heb_ctx *ctx, int rows);
+int heb_pack_rows(heb_ctx *ctx, const uint64_t *in, int64_t count, int rows, int64_t in_stride, uint64_t *out,
+                  void *stream);
+int heb_unpack_rows(heb_ctx *ctx, const uint64_t *in, int64_t count, int rows, uint64_t *out, int64_t out_stride,
+                    void *stream);
+
 /* --- instrumentation ---------------------------------------------------------------- */
 /* Enable (1) / disable (0) per-kernel CUDA-event timing; enabling clears old records. */
 int heb_prof_enable(int on);

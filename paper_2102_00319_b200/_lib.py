@@ -63,12 +63,16 @@ SIGNATURES: dict[str, list] = {
     "heb_conv_tensor": [_P, _CT, _CT, _CT, _I, _I, _I, _I, _I, _I, _I, _I, _P],
     "heb_sum_gather": [_P, _CT, _P, _I, _CT, _L, _I, _I, _P],
     "heb_gather": [_P, _CT, _P, _CT, _L, _I, _I, _P],
+    "heb_packed_words": [_P, _I],
+    "heb_pack_rows": [_P, _P, _L, _I, _L, _P, _P],
+    "heb_unpack_rows": [_P, _P, _L, _I, _P, _L, _P],
     "heb_prof_enable": [_I],
     "heb_prof_summary": [ctypes.c_char_p, ctypes.c_size_t],
     "heb_prof_next_bytes": [ctypes.c_double],
     "heb_bench_modmul": [_I, _I, _I, _U, ctypes.POINTER(ctypes.c_double), _P],
 }
-_RET = {"heb_last_error": ctypes.c_char_p, "heb_version": ctypes.c_int, "heb_ctx_ring_degree": ctypes.c_int}
+_RET = {"heb_last_error": ctypes.c_char_p, "heb_version": ctypes.c_int, "heb_ctx_ring_degree": ctypes.c_int,
+        "heb_packed_words": ctypes.c_int64}
 
 _lock = threading.Lock()
 _LIB: ctypes.CDLL | None = None

@@ -412,6 +412,29 @@ class B200Backend(HEBackend):
         buf = u64_to_dev(np.stack([c0, c1]), self.dev)
         return self._cipher(DevCipher(buf, level + 1), level, Fraction(scale), noise_bits)
 
+    # -- transport: bit-packed residue rows (csrc/packing.cu) -------------------------------
+    def packed_words(self, k: int) -> int:
+        """u64 words of one packed component (rows 0..k-1)."""
+        w = _lib.lib().heb_packed_words(self.ctx.handle, k)
+        if w < 0:
+            _lib.check(int(w), "heb_packed_words")
+        return int(w)
+
+    def pack_batch(self, batch: CipherBatch) -> "torch.Tensor":
+        """(B * 2 * packed_words(k),) int64 device tensor: the batch in wire format."""
+        k, B = batch.k, batch.count
+        out = torch.empty(B * 2 * self.packed_words(k), dtype=torch.int64, device=self.dev)
+        buf = batch.buf
+        if buf.stride(1) != buf.shape[2] * self.n or buf.stride(0) != 2 * buf.stride(1):
+            buf = buf.contiguous()
+        self.ctx.call("heb_pack_rows", buf.data_ptr(), B * 2, k, buf.stride(1), out.data_ptr(), self.ctx.stream)
+        return out
+
+    def unpack_into(self, packed: "torch.Tensor", out: "torch.Tensor", k: int) -> None:
+        """Wire format -> rows 0..k-1 of a (B, 2, K, N) device tensor."""
+        self.ctx.call("heb_unpack_rows", packed.data_ptr(), out.shape[0] * 2, k, out.data_ptr(), out.stride(1),
+                      self.ctx.stream)
+
     # -- serialization hooks (ckks.py:389-483) ----------------------------------------------
     # The payload format is the reference's: "<II" (k, N) then c0 and c1 as k x N
     # little-endian u64 standard-form coefficients.  Conversion runs on the device

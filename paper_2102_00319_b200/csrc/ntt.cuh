@@ -54,8 +54,8 @@ HD int lpos(int t, int m, int T) { return 2 * t + (m & 1) + 2 * T * (m >> 1); }
 
 template <int LOGN, int E = 16>
 struct Shape {
-    static_assert(E == 8 || E == 16, "8 or 16 elements per thread");
-    static constexpr int LOGE = E == 8 ? 3 : 4;
+    static_assert(E == 8 || E == 16 || E == 32, "8, 16 or 32 elements per thread");
+    static constexpr int LOGE = E == 8 ? 3 : (E == 16 ? 4 : 5);
     static constexpr int N = 1 << LOGN;
     static constexpr int T = N / E;
     static constexpr int REM = LOGN % LOGE;

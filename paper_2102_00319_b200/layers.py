@@ -357,7 +357,8 @@ class LayerEvaluator:
         return out
 
     def run_stream(self, enc: EncryptedNetworkBatch, host_inputs, level: int, scale: Fraction, noise: float,
-                   host_outputs, on_output=None, pipelines: int = 2, graphs: bool = True) -> None:
+                   host_outputs, on_output=None, pipelines: int = 2, graphs: bool = True,
+                   unpacked_shape: tuple | None = None) -> None:
         """Evaluate a sequence of pinned host input batches ((B, 2, K, N) int64 tensors).
 
         Batches are dealt round-robin to ``pipelines`` independent pipelines, each with
@@ -367,12 +368,24 @@ class LayerEvaluator:
         s are copied back into ``host_outputs[s]`` (pinned, (out, 2, k, N)).  On return
         the caller's current stream is ordered after all the work.  ``graphs``: replay
         one captured CUDA graph per pipeline instead of re-issuing every launch.
+        ``unpacked_shape``: the host inputs are in the bit-packed wire format
+        (``B200Backend.pack_batch``) of batches of this (B, 2, K, N) shape; they are
+        unpacked on the device, and the next copy of a pipeline overlaps its compute.
         """
         caller = torch.cuda.current_stream(self.be.dev)
         P = max(1, pipelines)
         comp = self._pipeline_streams("compute", P)
         copy = self._pipeline_streams("copy", P)
-        shape = tuple(host_inputs[0].shape)
+        packed = unpacked_shape is not None
+        shape = tuple(unpacked_shape) if packed else tuple(host_inputs[0].shape)
+        stage = [None] * P
+        if packed:
+            for p in range(P):
+                key = (("packed",) + tuple(host_inputs[0].shape), p)
+                if key not in self._inbufs:
+                    self._inbufs[key] = torch.empty(tuple(host_inputs[0].shape), dtype=host_inputs[0].dtype,
+                                                    device=self.be.dev)
+                stage[p] = self._inbufs[key]
         bufs = []
         for p in range(P):  # persistent per-pipeline device inputs (graph-captured addresses)
             b = self._inbufs.get((shape, p))
@@ -390,15 +403,19 @@ class LayerEvaluator:
             with torch.cuda.stream(copy[p]):
                 if s >= P:
                     copy[p].wait_event(consumed[p])
-                bufs[p].copy_(host_inputs[s], non_blocking=True)
+                (stage[p] if packed else bufs[p]).copy_(host_inputs[s], non_blocking=True)
                 copied[p].record(copy[p])
             with torch.cuda.stream(comp[p]):
                 comp[p].wait_event(copied[p])
+                if packed:
+                    self.be.unpack_into(stage[p], bufs[p], level + 1)
+                    consumed[p].record(comp[p])  # staging buffer free: next copy may start
                 if graphs:
                     out = self._replay(runners[p])
                 else:
                     out = self.run(enc, CipherBatch(bufs[p], level, scale, noise))
-                consumed[p].record(comp[p])
+                if not packed:
+                    consumed[p].record(comp[p])
                 host_outputs[s].copy_(out.buf[:, :, : out.k], non_blocking=True)
                 if on_output is not None:
                     on_output(s, out)

@@ -8,7 +8,7 @@ from conftest import REPO
 
 def _header_functions():
     text = open(os.path.join(REPO, "include", "heb200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(heb_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char \*)\s*(heb_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_entry_points():
