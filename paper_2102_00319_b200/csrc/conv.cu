@@ -16,19 +16,28 @@
 //     reference's canonical Montgomery residues exactly.
 #include "common.cuh"
 
+#include <cstdlib>
+
+static bool getenv_flag(const char *name) {
+    const char *v = getenv(name);
+    return v && *v && *v != '0';
+}
+
 namespace {
 constexpr int XC = 32;  // positions per CTA (one warp-width)
 constexpr int SW = 8;   // workers per position  -> 256 threads
 constexpr int FG = 5;   // filters per CTA group
 }  // namespace
 
-template <bool FLUSH>
-__global__ void __launch_bounds__(XC *SW, 2) k_conv_tensor(Ctx K, heb_ct A, heb_ct B, heb_ct D, int C, int m, int n,
-                                                            int F, int P, int Q, int s, int om, int on, int logn,
-                                                            int flush) {
-    extern __shared__ u64 wsm[];  // [tap][fl][comp][XC]
+// One CTA = (row r, XC positions from bx * XC, filter group): integer rows (and, without
+// the split-limb path, FP64 rows with one exact FP64 modular product per term).
+template <bool FLUSH, bool ALLOW_FP>
+__device__ __forceinline__ void conv_body(u64 *wsm, const Ctx &K, const heb_ct &A, const heb_ct &B, const heb_ct &D,
+                                          int C, int m, int n, int F, int P, int Q, int s, int om, int on, int logn,
+                                          int flush, int bx) {
+    // wsm: [tap][fl][comp][XC]
     const int xl = threadIdx.x % XC, w = threadIdx.x / XC;
-    const int x = blockIdx.x * XC + xl;
+    const int x = bx * XC + xl;
     const int r = blockIdx.y;
     const int f0 = blockIdx.z * FG;
     const int nf = min(FG, F - f0);
@@ -43,7 +52,7 @@ __global__ void __launch_bounds__(XC *SW, 2) k_conv_tensor(Ctx K, heb_ct A, heb_
         const int64_t widx = (int64_t)(f0 + fl) * taps + tap;
         const u64 *src = B.data + widx * B.ct_stride + roff;
         u64 *dst = wsm + ((size_t)(tap * FG + fl) * 2) * XC + xl;
-        if (Pr.use_fp) {  // FP64 rows: stage the weights as doubles
+        if (ALLOW_FP && Pr.use_fp) {  // FP64 rows: stage the weights as doubles
             dst[0] = (u64)__double_as_longlong(ntt::u2d(src[0]));
             dst[XC] = (u64)__double_as_longlong(ntt::u2d(src[B.comp_stride]));
         } else {
@@ -54,7 +63,7 @@ __global__ void __launch_bounds__(XC *SW, 2) k_conv_tensor(Ctx K, heb_ct A, heb_
     __syncthreads();
 
     const int cells = om * on;
-    if (Pr.use_fp) {
+    if (ALLOW_FP && Pr.use_fp) {
         // Rows with p < 2^42: every product reduced exactly on the FP64 pipe (6 ops),
         // sums exact below 2^47; one R^-1 product per output restores the Montgomery
         // factor of the reference's mont_mul accumulation.
@@ -157,6 +166,138 @@ __global__ void __launch_bounds__(XC *SW, 2) k_conv_tensor(Ctx K, heb_ct A, heb_
     }
 }
 
+// ---------------------------------------------------------------------------------
+// FP64 rows (p < 2^42): split-limb products.  Every residue is split into 20-bit limbs
+// (a = a_h 2^20 + a_l), so each limb product is < 2^42 and is accumulated EXACTLY by
+// one DFMA -- no per-product modular reduction.  A Karatsuba component costs 4 DFMA
+// (hh, the two cross terms into one accumulator, ll) instead of a 6-op exact FP64
+// modular product plus an add; the three partial sums of each component are reduced
+// once per output cell.  Bounds: limbs of the component sums < 2^21, so every term is
+// < 2^42 and a sum of `taps` terms stays below 2^53 for taps <= 256.  The weight limbs
+// are staged in shared memory as doubles ([tap][filter][b0h, b0l, b1h, b1l][XF]).
+namespace {
+constexpr int XF = 16;  // positions per CTA
+constexpr int SF = 16;  // workers per position -> 256 threads
+#ifndef CONV_FGF
+#define CONV_FGF 5
+#endif
+constexpr int FGF = CONV_FGF;  // filters per CTA group
+constexpr int FP_MAX_TAPS = 256;
+constexpr u64 M20 = (1ull << 20) - 1;
+}  // namespace
+
+__device__ __forceinline__ void conv_body_limbs(double *wl, const Ctx &K, const heb_ct &A, const heb_ct &B,
+                                                const heb_ct &D, int C, int m, int n, int F, int P, int Q, int s,
+                                                int om, int on, int logn) {
+    const int xl = threadIdx.x % XF, w = threadIdx.x / XF;
+    const int x = blockIdx.x * XF + xl;
+    const int r = blockIdx.y;
+    const PrimeInfo Pr = K.pi[r];
+    const int f0 = blockIdx.z * FGF;
+    const int nf = min(FGF, F - f0);
+    const int taps = C * P * Q;
+    const int64_t roff = ((int64_t)r << logn) + x;
+    for (int e = w; e < taps * nf; e += SF) {
+        const int tap = e / nf, fl = e % nf;
+        const u64 *src = B.data + ((int64_t)(f0 + fl) * taps + tap) * B.ct_stride + roff;
+        const u64 b0 = src[0], b1 = src[B.comp_stride];
+        double *dst = wl + (size_t)(tap * FGF + fl) * 4 * XF + xl;
+        dst[0] = ntt::u2d(b0 >> 20);
+        dst[XF] = ntt::u2d(b0 & M20);
+        dst[2 * XF] = ntt::u2d(b1 >> 20);
+        dst[3 * XF] = ntt::u2d(b1 & M20);
+    }
+    __syncthreads();
+    const double pd = Pr.pd, pinvd = Pr.pinvd;
+    // limb weights with the Montgomery correction folded in: R^-1 * (2^40, 2^20, 1)
+    const double c0 = (double)Pr.rinv;
+    const double c20 = (double)ntt::fcanon(ntt::fmul(1048576.0, c0, pd, pinvd), pd, pinvd);
+    const double c40 = (double)ntt::fcanon(ntt::fmul(1048576.0, c20, pd, pinvd), pd, pinvd);
+    const int cells = om * on;
+    for (int cell = w; cell < cells; cell += SF) {
+        const int i = cell / on, j = cell % on;
+        double h0[FGF], q0[FGF], l0[FGF], h1[FGF], q1[FGF], l1[FGF], h2[FGF], q2[FGF], l2[FGF];
+#pragma unroll
+        for (int fl = 0; fl < FGF; ++fl) h0[fl] = q0[fl] = l0[fl] = h1[fl] = q1[fl] = l1[fl] = h2[fl] = q2[fl] = l2[fl] = 0.0;
+        // taps in (c, p, q) order; the next tap's inputs are loaded before this tap's math
+        const u64 *base = A.data + ((int64_t)(i * s) * n + j * s) * A.ct_stride + roff;
+        int c = 0, pp = 0, qq = 0;
+        u64 na0 = __ldg(base), na1 = __ldg(base + A.comp_stride);
+        for (int tap = 0; tap < taps; ++tap) {
+            {
+                const u64 a0 = na0, a1 = na1;
+                if (++qq == Q) {
+                    qq = 0;
+                    if (++pp == P) {
+                        pp = 0;
+                        ++c;
+                    }
+                }
+                if (tap + 1 < taps) {
+                    const u64 *ap = base + ((int64_t)c * m * n + (int64_t)pp * n + qq) * A.ct_stride;
+                    na0 = __ldg(ap);
+                    na1 = __ldg(ap + A.comp_stride);
+                }
+                {
+                    const double a0h = ntt::u2d(a0 >> 20), a0l = ntt::u2d(a0 & M20);
+                    const double a1h = ntt::u2d(a1 >> 20), a1l = ntt::u2d(a1 & M20);
+                    const double ash = a0h + a1h, asl = a0l + a1l;
+                    const double *wt = wl + (size_t)(tap * FGF) * 4 * XF + xl;
+#pragma unroll
+                    for (int fl = 0; fl < FGF; ++fl) {
+                        if (fl < nf) {
+                            const double b0h = wt[(4 * fl) * XF], b0l = wt[(4 * fl + 1) * XF];
+                            const double b1h = wt[(4 * fl + 2) * XF], b1l = wt[(4 * fl + 3) * XF];
+                            const double bsh = b0h + b1h, bsl = b0l + b1l;
+                            h0[fl] = fma(a0h, b0h, h0[fl]);
+                            q0[fl] = fma(a0h, b0l, fma(a0l, b0h, q0[fl]));
+                            l0[fl] = fma(a0l, b0l, l0[fl]);
+                            h2[fl] = fma(a1h, b1h, h2[fl]);
+                            q2[fl] = fma(a1h, b1l, fma(a1l, b1h, q2[fl]));
+                            l2[fl] = fma(a1l, b1l, l2[fl]);
+                            h1[fl] = fma(ash, bsh, h1[fl]);
+                            q1[fl] = fma(ash, bsl, fma(asl, bsh, q1[fl]));
+                            l1[fl] = fma(asl, bsl, l1[fl]);
+                        }
+                    }
+                }
+            }
+        }
+        auto comb = [&](double h, double q, double l) {
+            return ntt::fmul(ntt::fred(h, pd, pinvd), c40, pd, pinvd) + ntt::fmul(ntt::fred(q, pd, pinvd), c20, pd, pinvd) +
+                   ntt::fmul(ntt::fred(l, pd, pinvd), c0, pd, pinvd);
+        };
+#pragma unroll
+        for (int fl = 0; fl < FGF; ++fl) {
+            if (fl < nf) {
+                const double e0 = comb(h0[fl], q0[fl], l0[fl]);
+                const double e2 = comb(h2[fl], q2[fl], l2[fl]);
+                const double e1 = comb(h1[fl], q1[fl], l1[fl]) - e0 - e2;
+                u64 *dp = D.data + ((int64_t)(f0 + fl) * cells + cell) * D.ct_stride + roff;
+                dp[0] = ntt::fcanon(e0, pd, pinvd);
+                dp[D.comp_stride] = ntt::fcanon(e1, pd, pinvd);
+                dp[2 * D.comp_stride] = ntt::fcanon(e2, pd, pinvd);
+            }
+        }
+    }
+}
+
+// One launch for all rows: FP64 rows take the split-limb body (XF positions per CTA),
+// integer rows the 128-bit body (XC positions per CTA; the surplus x-blocks exit), so
+// the long integer-row CTAs run alongside the FP64-row CTAs.
+template <bool FLUSH, bool LIMBS>
+__global__ void __launch_bounds__(256, 2) k_conv_tensor(Ctx K, heb_ct A, heb_ct B, heb_ct D, int C, int m, int n,
+                                                         int F, int P, int Q, int s, int om, int on, int logn,
+                                                         int flush) {
+    extern __shared__ u64 conv_smem[];
+    if (LIMBS && K.pi[blockIdx.y].use_fp) {
+        conv_body_limbs(reinterpret_cast<double *>(conv_smem), K, A, B, D, C, m, n, F, P, Q, s, om, on, logn);
+        return;
+    }
+    if (LIMBS && (int)blockIdx.x >= ((1 << logn) / XC)) return;
+    conv_body<FLUSH, !LIMBS>(conv_smem, K, A, B, D, C, m, n, F, P, Q, s, om, on, logn, flush, blockIdx.x);
+}
+
 extern "C" int heb_conv_tensor(heb_ctx *c, heb_ct a, heb_ct b, heb_ct d, int channels, int m, int n, int filters,
                                int kp, int kq, int stride, int k, void *stream) {
     if (!c || channels < 1 || filters < 1 || kp < 1 || kq < 1 || stride < 1 || kp > m || kq > n || k < 1 ||
@@ -168,20 +309,25 @@ extern "C" int heb_conv_tensor(heb_ctx *c, heb_ct a, heb_ct b, heb_ct d, int cha
     if (sm > 220 * 1024) return fail(HEB_EUNSUP, "heb_conv_tensor: %d taps exceed the shared-memory stage", taps);
     cudaStream_t st = (cudaStream_t)stream;
     const bool need_flush = taps > c->flush;
-    CUDA_TRY(prep_kernel(k_conv_tensor<true>, sm));
-    CUDA_TRY(prep_kernel(k_conv_tensor<false>, sm));
-    dim3 grid(c->n / XC, k, (filters + FG - 1) / FG);
+    const bool limbs = taps <= FP_MAX_TAPS && !getenv_flag("HEB_CONV_NO_LIMBS");
+    const size_t smf = sizeof(double) * (size_t)taps * FGF * 4 * XF;
+    const size_t smem = limbs ? std::max(sm, smf) : sm;
+    const dim3 grid(c->n / (limbs ? XF : XC), k, (filters + FG - 1) / FG);
+    static_assert(FG == FGF, "both bodies use the same filter groups");
     const double nout = (double)filters * om * on;
-    {
-        PROF("k_conv_tensor", st,
-             8.0 * c->n * k * (2.0 * channels * m * n + 2.0 * filters * taps + 3.0 * nout));
-        if (need_flush)
-            k_conv_tensor<true><<<grid, XC * SW, sm, st>>>(kctx(c), a, b, d, channels, m, n, filters, kp, kq, stride,
-                                                           om, on, c->log_n, c->flush);
-        else
-            k_conv_tensor<false><<<grid, XC * SW, sm, st>>>(kctx(c), a, b, d, channels, m, n, filters, kp, kq, stride,
-                                                            om, on, c->log_n, c->flush);
+    PROF("k_conv_tensor", st, 8.0 * c->n * k * (2.0 * channels * m * n + 2.0 * filters * taps + 3.0 * nout));
+#define CONV_LAUNCH(FL, LI)                                                                                   \
+    {                                                                                                         \
+        CUDA_TRY(prep_kernel(k_conv_tensor<FL, LI>, smem));                                                   \
+        k_conv_tensor<FL, LI><<<grid, 256, smem, st>>>(kctx(c), a, b, d, channels, m, n, filters, kp, kq, stride, \
+                                                       om, on, c->log_n, c->flush);                          \
     }
+    if (limbs) {
+        if (need_flush) CONV_LAUNCH(true, true) else CONV_LAUNCH(false, true)
+    } else {
+        if (need_flush) CONV_LAUNCH(true, false) else CONV_LAUNCH(false, false)
+    }
+#undef CONV_LAUNCH
     LAUNCH_CHECK();
     return HEB_OK;
 }
