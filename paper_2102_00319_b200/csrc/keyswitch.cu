@@ -326,32 +326,94 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_down_head(Ctx K, const u64 *acc, heb_ct d,
     }
 }
 
+// exact FP64 helpers for the tail's FP64 rows (p < 2^42)
+__device__ __forceinline__ double fp_imul(i64 a, double w, double w32, double pd, double pinvd) {
+    // a (any signed 64-bit) * w mod p, as (a >> 32) * (2^32 w) + (a & (2^32-1)) * w
+    const double hi = (double)(int)(a >> 32), lo = (double)(u32)(a & 0xffffffffu);
+    return ntt::fmul(hi, w32, pd, pinvd) + ntt::fmul(lo, w, pd, pinvd);
+}
+
+// ModDown head for the rescale path, after k_ks_down_head has stored
+// aP = center(INTT_P(acc_P)); one CTA per (item, component):
+//   cL = center((INTT_L(acc_L + P d_L) - aP) P^-1 mod q_L)
+// cL depends only on (item, component, position); computing it here once (instead of
+// in each of the k-1 tail rows) removes most of the tail's integer prologue.
 template <int LOGN>
-__global__ void ROW_BOUNDS(LOGN) k_ks_down_rescale_tail(Ctx K, const u64 *acc, heb_ct d,
-                                                                                const i64 *aP, const u64 *bL, int k,
-                                                                                heb_ct out, int64_t count) {
+__global__ void ROW_BOUNDS(LOGN) k_ks_down_head_cl(Ctx K, const u64 *acc, heb_ct d, int k, const i64 *aP, i64 *cL,
+                                                   int64_t count) {
+    extern __shared__ u64 sm[];
+    const int c = blockIdx.z;
+    const int n = 1 << LOGN;
+    const int pos = tpos<LOGN>();
+    const int L = k - 1;
+    const PrimeInfo PL = K.pi[L];
+    const LevelConst C = K.lc[(size_t)L * K.num_rows + L];
+    for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
+        const i64 *ap = aP + (b * 2 + c) * n;
+        i64 *cl = cL + (b * 2 + c) * n;
+        u64 x[16], y[16];
+        load16<LOGN>(acc + ((b * 2 + c) * (k + 1) + L) * n + pos, x);
+        load16<LOGN>(at(d, b, c, L, LOGN) + pos, y);
+#pragma unroll
+        for (int m = 0; m < 16; ++m) x[m] = add_mod(x[m], shoup(y[m], C.pmod.x, C.pmod.y, PL.p), PL.p);
+        inv_any<LOGN>(K, L, PL, sm, x,
+                      [&](int i, u64 v) {
+                          const u64 sl = sub_mod(shoup(v, C.pinv.x, C.pinv.y, PL.p),
+                                                 signed_mul_const(__ldcg(ap + i), C.pinv.x, C.pinv.y, PL.p), PL.p);
+                          cl[i] = center(sl, PL.p);
+                      },
+                      true);
+    }
+}
+
+template <int LOGN>
+__global__ void ROW_BOUNDS(LOGN) k_ks_down_rescale_tail(Ctx K, const u64 *acc, heb_ct d, const i64 *aP, const i64 *cL,
+                                                        int k, heb_ct out, int64_t count) {
     extern __shared__ u64 sm[];
     const int i = lbx<LOGN>(), c = blockIdx.z;
     const int n = 1 << LOGN;
     const int pos = tpos<LOGN>();
     const int L = k - 1;
     const PrimeInfo Pi = K.pi[i];
-    const PrimeInfo PL = K.pi[L];
     const LevelConst Ci = K.lc[(size_t)L * K.num_rows + i];  // level L: drop q_L
-    const LevelConst CL = K.lc[(size_t)L * K.num_rows + L];  // P^-1 mod q_L
+    if (HEB_FPSEL(Pi.use_fp)) {
+        // FP64 row: every product is an exact FP64 modular product (the integer pipe is
+        // this kernel's bottleneck otherwise)
+        const double pd = Pi.pd, pinvd = Pi.pinvd;
+        const double ar = (double)Ci.alpha_r.x, br = (double)Ci.beta_r.x;
+        const double ar32 = (double)ntt::fcanon(ntt::fmul(4294967296.0, ar, pd, pinvd), pd, pinvd);
+        const double al = (double)Ci.alpha.x, be = (double)Ci.beta.x;
+        for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
+            const i64 *ap = aP + (b * 2 + c) * n;
+            const i64 *cl = cL + (b * 2 + c) * n;
+            u64 y[16];
+            fwd_any<LOGN>(K, i, Pi, sm,
+                          [&](int j) {
+                              const double v = fp_imul(__ldcg(ap + j), ar, ar32, pd, pinvd) +
+                                               ntt::fmul((double)__ldcg(cl + j), br, pd, pinvd);
+                              return ntt::fcanon(v, pd, pinvd);
+                          },
+                          y);
+            u64 x[16], z[16];
+            load16<LOGN>(acc + ((b * 2 + c) * (k + 1) + i) * n + pos, x);
+            load16<LOGN>(at(d, b, c, i, LOGN) + pos, z);
+#pragma unroll
+            for (int m = 0; m < 16; ++m)
+                x[m] = ntt::fcanon(ntt::fmul(ntt::u2d(x[m]), al, pd, pinvd) + ntt::fmul(ntt::u2d(z[m]), be, pd, pinvd) -
+                                       ntt::u2d(y[m]),
+                                   pd, pinvd);
+            store16<LOGN>(at(out, b, c, i, LOGN) + pos, x);
+        }
+        return;
+    }
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         const i64 *ap = aP + (b * 2 + c) * n;
-        const u64 *bl = bL + (b * 2 + c) * n;
+        const i64 *cl = cL + (b * 2 + c) * n;
         u64 y[16];
         fwd_any<LOGN>(K, i, Pi, sm,
             [&](int j) {
-                const i64 a = __ldcg(ap + j);
-                // s_L = (bL - aP) * P^-1 mod q_L, centred
-                const u64 sl = sub_mod(shoup(__ldcg(bl + j), CL.pinv.x, CL.pinv.y, PL.p),
-                                       signed_mul_const(a, CL.pinv.x, CL.pinv.y, PL.p), PL.p);
-                const i64 cl = center(sl, PL.p);
-                return add_mod(signed_mul_const(a, Ci.alpha_r.x, Ci.alpha_r.y, Pi.p),
-                               signed_mul_const(cl, Ci.beta_r.x, Ci.beta_r.y, Pi.p), Pi.p);
+                return add_mod(signed_mul_const(__ldcg(ap + j), Ci.alpha_r.x, Ci.alpha_r.y, Pi.p),
+                               signed_mul_const(__ldcg(cl + j), Ci.beta_r.x, Ci.beta_r.y, Pi.p), Pi.p);
             },
             y);
         u64 x[16], z[16];
@@ -403,6 +465,7 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
     CUDA_TRY(prep_kernel(k_ks_head<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_ks_modup_ntt<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_ks_down_head<LOGN>, sm));
+    CUDA_TRY(prep_kernel(k_ks_down_head_cl<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_ks_down_rescale_tail<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_ks_down_tail<LOGN>, sm));
     const int k = level + 1, n = c->n;
@@ -450,11 +513,14 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
             LAUNCH_CHECK();
         }
         if (rescale) {
-            { PROF("k_ks_down_head", st, 8.0 * n * cnt * 10.0); CUDA_TRY(launch_rows<LOGN>(k_ks_down_head<LOGN>, dim3(dim3(2, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
-                                                                 (u64 *)sL.p, cnt)); }
+            { PROF("k_ks_down_head", st, 8.0 * n * cnt * 4.0); CUDA_TRY(launch_rows<LOGN>(k_ks_down_head<LOGN>, dim3(dim3(1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
+                                                                 (u64 *)nullptr, cnt)); }
+            LAUNCH_CHECK();
+            { PROF("k_ks_down_head_cl", st, 8.0 * n * cnt * 2.0 * 4.0); CUDA_TRY(launch_rows<LOGN>(k_ks_down_head_cl<LOGN>, dim3(dim3(1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd, k, (const i64 *)sP.p,
+                                                                 (i64 *)sL.p, cnt)); }
             LAUNCH_CHECK();
             { PROF("k_ks_down_rescale_tail", st, 8.0 * n * cnt * 2.0 * (2 + 3 * (k - 1))); CUDA_TRY(launch_rows<LOGN>(k_ks_down_rescale_tail<LOGN>, dim3(dim3(k - 1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd,
-                                                                             (const i64 *)sP.p, (const u64 *)sL.p, k,
+                                                                             (const i64 *)sP.p, (const i64 *)sL.p, k,
                                                                              o, cnt)); }
             LAUNCH_CHECK();
         } else {
