@@ -316,13 +316,14 @@ def run_gpu(args) -> None:
                 "frac_of_hbm": round(path_rate / peaks["hbm_gbs"], 4),
                 "source": "SURVEY.md §8(d) cfg2 layer-wise compulsory bytes",
             },
-            "int_roofline": None if (peak_mm is None or args.config != "cfg2") else {
+            "modmul_rate": None if (peak_mm is None or args.config != "cfg2") else {
                 "modmuls_per_batch": CFG2_MODMULS_PER_BATCH,
                 "achieved_modmul_per_s": CFG2_MODMULS_PER_BATCH * value / batch,
-                "peak_modmul_per_s": peak_mm,
-                "frac": round(CFG2_MODMULS_PER_BATCH * value / batch / peak_mm, 4),
-                "peak_source": "heb_bench_modmul Shoup microbenchmark on this GPU",
+                "shoup_int_peak_per_s": peak_mm,
+                "note": "SURVEY 8(d) modmul count; the 40-bit rows run on the FP64 (DFMA) pipe, "
+                        "so the integer Shoup peak is not an upper bound for the mix",
             },
+            "compute_roofline": ncu_pipes(name),
             "kernels": {k: {"launches": v[0], "ms": round(v[1], 3), "gbs": round(v[2] / max(v[1], 1e-9) / 1e6, 1)}
                         for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
             "cpu_baseline": cpu,
@@ -411,6 +412,19 @@ def ncu_traffic(kernel: str):
         d = json.load(fh)
     rec = d.get(kernel)
     return rec.get("dram_bytes_per_launch") if rec else None
+
+
+def ncu_pipes(kernel: str):
+    """Pipe utilisation of the top kernel from the committed ncu --set full capture."""
+    path = os.path.join(REPO, "profiles", "ncu_top_kernel.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        rec = json.load(fh).get(kernel)
+    if not rec:
+        return None
+    keys = ("fp64_pipe_pct", "alu_pipe_pct", "fma_pipe_pct", "issue_active_pct", "source")
+    return {k: rec[k] for k in keys if k in rec}
 
 
 # ---------------------------------------------------------------------------
