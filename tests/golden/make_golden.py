@@ -67,6 +67,76 @@ def make_backend(m, L, r, seed, extra):
     return be
 
 
+def ref_rotate(be, ct, steps: int):
+    """Rotation built ONLY from the reference's own machinery (SURVEY.md §8c rotation
+    oracle): a Galois key generated exactly like keygen's evk loop (ckks.py:151-176)
+    with s^2 replaced by s(X^g) and the sampler tagged (seed, 5, g), the automorphism
+    applied in the coefficient domain with the reference NTT kernels, and the key
+    switch done by relin_accumulate + moddown_special (ckks.py:359-387) without the
+    rescale.  Returns (galois key b digest, c0, c1)."""
+    ch, n = be.chain, be.n
+    g = pow(5, steps % (n // 2), 2 * n)
+    s = be._sample_ternary(be._rng(1))  # keygen's secret
+    t = np.zeros(n, dtype=np.int64)
+    for i in range(n):
+        j = (i * g) % (2 * n)
+        if j < n:
+            t[j] += s[i]
+        else:
+            t[j - n] -= s[i]
+    s_eval = be._coeffs_to_all_rows(s)
+    target = be._coeffs_to_all_rows(t)
+    rows_all, digits = ch.num_rows, ch.num_rows - 1
+    rng = be._rng(5, g)
+    gk_a = np.empty((digits, rows_all, n), dtype=np.uint64)
+    gk_b = np.empty_like(gk_a)
+    for j in range(digits):
+        gk_a[j] = be._sample_uniform_rows(rng, rows_all)
+        e_j = be._coeffs_to_all_rows(be._sample_gaussian(rng))
+        bj = gk_b[j]
+        ref_kernels.mul_rows(gk_a[j], s_eval, ch.p, ch.p_inv, bj)
+        ref_kernels.neg_rows(bj, ch.p, bj)
+        ref_kernels.add_rows(bj, e_j, ch.p, bj)
+        q_j = int(ch.p[j])
+        factor = (ch.special_prime % q_j) * ((1 << 64) % q_j) % q_j
+        term = np.empty((1, n), dtype=np.uint64)
+        ref_kernels.scalar_mul_rows(target[j:j + 1], np.array([factor], dtype=np.uint64), ch.p[j:j + 1],
+                                    ch.p_inv[j:j + 1], term)
+        ref_kernels.add_rows(bj[j:j + 1], term, ch.p[j:j + 1], bj[j:j + 1])
+    k = ct.level + 1
+
+    def sigma(rows):
+        c = rows.copy()
+        ref_kernels.ntt_inv_rows(c, ch.twiddles[:k], ch.n_inv[:k], ch.p[:k], ch.p_inv[:k])
+        out = np.zeros_like(c)
+        for i in range(n):
+            j = (i * g) % (2 * n)
+            if j < n:
+                out[:, j] = c[:, i]
+            else:
+                out[:, j - n] = np.where(c[:, i] == 0, 0, ch.p[:k] - c[:, i])
+        ref_kernels.ntt_fwd_rows(out, ch.twiddles[:k], ch.p[:k], ch.p_inv[:k])
+        return out
+
+    c0r, c1r = sigma(ct.payload.c0), sigma(ct.payload.c1)
+    d2_coeff = c1r.copy()
+    ref_kernels.ntt_inv_rows(d2_coeff, ch.twiddles[:k], ch.n_inv[:k], ch.p[:k], ch.p_inv[:k])
+    ref_kernels.from_mont_rows(d2_coeff, ch.p[:k], ch.p_inv[:k])
+    d2_cent = np.empty((k, n), dtype=np.int64)
+    ref_kernels.centered_rows(d2_coeff, ch.p[:k], d2_cent)
+    acc0 = np.zeros((k + 1, n), dtype=np.uint64)
+    acc1 = np.zeros_like(acc0)
+    sp = ch.special_row
+    ref_kernels.relin_accumulate(c1r, d2_cent, gk_b, gk_a, sp, ch.twiddles, ch.p, ch.p_inv, ch.r2, acc0, acc1)
+    rel0 = np.empty((k, n), dtype=np.uint64)
+    rel1 = np.empty_like(rel0)
+    sp_inv = be._special_inv[ct.level]
+    ref_kernels.moddown_special(acc0, sp, ch.twiddles, ch.n_inv, ch.p, ch.p_inv, ch.r2, sp_inv, rel0)
+    ref_kernels.moddown_special(acc1, sp, ch.twiddles, ch.n_inv, ch.p, ch.p_inv, ch.r2, sp_inv, rel1)
+    ref_kernels.add_rows(rel0, c0r, ch.p[:k], rel0)
+    return digest(gk_b), rel0, rel1
+
+
 def frac(x: Fraction) -> str:
     return f"{x.numerator}/{x.denominator}"
 
@@ -141,6 +211,13 @@ def small_ring(golden: dict) -> dict:
     arrays["record_fin"] = np.frombuffer(ref_ser.cipher_record(be, fin), dtype=np.uint8)
     arrays["envelope_fin"] = np.frombuffer(ref_ser.wrap(ref_ser.KIND_CIPHER, be, ref_ser.cipher_record(be, fin)),
                                            dtype=np.uint8)
+    # rotation pinned on the reference's own kernels (no reference API exists for it)
+    rot_meta = {}
+    for steps in (1, 3):
+        gdig, r0, r1 = ref_rotate(be, a, steps)
+        arrays[f"rot{steps}_c0"], arrays[f"rot{steps}_c1"] = r0, r1
+        rot_meta[str(steps)] = {"galois_key_b": gdig, "level": a.level}
+    golden_rot = rot_meta
     kp = be.key_payload_bytes(keys)
     key_digests = {role: hashlib.sha256(data).hexdigest() for role, data in kp.items()}
     golden["s128"] = {
@@ -150,6 +227,7 @@ def small_ring(golden: dict) -> dict:
         "ctpt": {"level": ctpt.level, "scale": frac(ctpt.scale), "noise": ctpt.noise_bits},
         "counters": be.counters.snapshot().__dict__,
         "key_payload_sha256": key_digests,
+        "rotation": golden_rot,
         "payload_meta": {"a": [a.level, frac(a.scale), a.noise_bits], "fin": [fin.level, frac(fin.scale), fin.noise_bits],
                          "a3": [a3.level, frac(a3.scale), a3.noise_bits]},
     }

@@ -151,6 +151,21 @@ class TestS128:
         olvl2 = ob.rotate(ob.drop_to_level(oct_, 2), 1)
         assert np.array_equal(host(be, lvl2)[0], olvl2.payload.c0)
 
+    @pytest.mark.parametrize("steps", [1, 3])
+    def test_rotation_matches_reference_kernels(self, s128, golden, steps):
+        """Device rotation against the reference-kernel rotation fixture (make_golden.ref_rotate)."""
+        from paper_2102_00319_b200.backend import B200Backend
+
+        be = B200Backend(s128_params(), S128["extra"])
+        keys = be.keygen(galois_steps=(steps,))
+        be.set_eval_key(keys)
+        rec = golden["s128"]["rotation"][str(steps)]
+        g = be.galois_element(steps)
+        assert digest(keys.galois[g].b.cpu().numpy().view(np.uint64)) == rec["galois_key_b"]
+        ct = be.cipher_from_host(s128["a_c0"], s128["a_c1"], rec["level"], be.canonical_scale, 0.0)
+        c0, c1 = be.cipher_rows_host(be.rotate(ct, steps))
+        assert np.array_equal(c0, s128[f"rot{steps}_c0"]) and np.array_equal(c1, s128[f"rot{steps}_c1"])
+
     @pytest.mark.parametrize("name", ["mini2", "mini3", "mini4"])
     def test_mini_cnn_percell_matches_reference(self, golden, dev_s128, name):
         from nets import mini_networks

@@ -181,3 +181,24 @@ def test_cfg1_ops_match_reference_digests(golden):
         assert cd(be.mul_ct_pt(x, be.encode_plain(ys[i], level=x.level))) == rec["ctpt"]
         assert cd(be.add_ct_ct(x, y)) == rec["add"]
         assert np.allclose(be.decrypt(mul, keys).values[:8], rec["mul_dec8"], atol=0, rtol=0)
+
+
+class TestRotationPinned:
+    """Rotation has no reference API; tests/golden/make_golden.py builds it from the
+    reference's own keygen loop and kernels (relin_accumulate + moddown_special), so
+    the oracle's rotation is pinned to reference arithmetic, not only to itself."""
+
+    @pytest.mark.parametrize("steps", [1, 3])
+    def test_rotation_matches_reference_kernels(self, s128, golden, steps):
+        from oracle.ckks_oracle import OracleBackend, _Cipher
+
+        be = OracleBackend(s128_params(), S128["extra"])
+        keys = be.keygen(galois_steps=(steps,))
+        be.set_eval_key(keys)
+        g = be.galois_element(steps)
+        rec = golden["s128"]["rotation"][str(steps)]
+        assert digest(keys.galois[g][0]) == rec["galois_key_b"]
+        ct = be._cipher(_Cipher(s128["a_c0"], s128["a_c1"]), rec["level"], be.canonical_scale, 0.0)
+        rot = be.rotate(ct, steps)
+        assert np.array_equal(rot.payload.c0, s128[f"rot{steps}_c0"])
+        assert np.array_equal(rot.payload.c1, s128[f"rot{steps}_c1"])
