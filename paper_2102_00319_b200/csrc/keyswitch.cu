@@ -170,6 +170,164 @@ __global__ void ROW_BOUNDS(LOGN)
     }
 }
 
+// ---------------------------------------------------------------------------------
+// Fused ModUp with the accumulators in tensor memory (TMEM).
+// One CTA per (item, target t): for every digit j it forms v_j = NTT_t(D_j mod p_t R)
+// (v_t = d2_t needs no transform) and accumulates v_j (*) key_b[j][t] and
+// v_j (*) key_a[j][t] for its 16 positions per thread.  The two accumulators (32 words
+// per position pair... 64 32-bit columns per thread) live in TMEM: 256 columns per CTA,
+// warp w owns lane quadrant w % 4 and column group w / 4, so two CTAs (1024 threads)
+// fit one SM's 512 columns and the NTT keeps its full register budget.  No ModUp
+// intermediate ever reaches HBM and the separate MAC pass disappears.
+// Column map per thread: component c, position m -> columns 32 c + 2 m (+1): the 64-bit
+// accumulator (FP64 rows: an exact double sum; integer rows: a u64 in [0, 2p)).
+__device__ __forceinline__ void tmem_st8(uint32_t a, const uint32_t (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(a), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t a, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(a)
+                 : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// accumulate y (*) key over this thread's 16 line-pair positions, 4 positions per TMEM access
+template <int LOGN, bool FP>
+__device__ __forceinline__ void modup_acc(uint32_t ta, const u64 (&y)[16], const ulonglong2 *keyrow, int pos,
+                                          bool first, const PrimeInfo &P) {
+    const int n = 1 << LOGN;
+    constexpr int T = KT<LOGN>;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // positions m = 4q .. 4q+3 = pairs 2q, 2q+1
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            uint32_t w[8];
+            if (!first) tmem_ld8(ta + 32 * c + 8 * q, w);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int i = 2 * q + h;  // pair index: positions pos + 2T i (+1)
+                const int off = pos + 2 * T * i;
+                if constexpr (FP) {
+                    const double *kd = reinterpret_cast<const double *>(keyrow) + (size_t)c * n;
+                    const double2 kv = __ldg(reinterpret_cast<const double2 *>(kd + off));
+                    double a0 = ntt::fmul(ntt::u2d(y[2 * i]), kv.x, P.pd, P.pinvd);
+                    double a1 = ntt::fmul(ntt::u2d(y[2 * i + 1]), kv.y, P.pd, P.pinvd);
+                    if (!first) {
+                        a0 += __hiloint2double(w[4 * h + 1], w[4 * h]);
+                        a1 += __hiloint2double(w[4 * h + 3], w[4 * h + 2]);
+                    }
+                    w[4 * h] = __double2loint(a0);
+                    w[4 * h + 1] = __double2hiint(a0);
+                    w[4 * h + 2] = __double2loint(a1);
+                    w[4 * h + 3] = __double2hiint(a1);
+                } else {
+                    const ulonglong2 *kp = keyrow + (size_t)c * n + off;
+                    const ulonglong2 k0 = __ldg(kp), k1 = __ldg(kp + 1);
+                    u64 a0 = shoup_lazy(y[2 * i], k0.x, k0.y, P.p);
+                    u64 a1 = shoup_lazy(y[2 * i + 1], k1.x, k1.y, P.p);
+                    if (!first) {
+                        a0 = csub(a0 + ((u64)w[4 * h + 1] << 32 | w[4 * h]), 2 * P.p);
+                        a1 = csub(a1 + ((u64)w[4 * h + 3] << 32 | w[4 * h + 2]), 2 * P.p);
+                    }
+                    w[4 * h] = (uint32_t)a0;
+                    w[4 * h + 1] = (uint32_t)(a0 >> 32);
+                    w[4 * h + 2] = (uint32_t)a1;
+                    w[4 * h + 3] = (uint32_t)(a1 >> 32);
+                }
+            }
+            tmem_st8(ta + 32 * c + 8 * q, w);
+        }
+    }
+    tmem_wait_st();
+}
+
+template <int LOGN, bool FP>
+__device__ __forceinline__ void modup_store(uint32_t ta, u64 *o0, u64 *o1, int pos, const PrimeInfo &P) {
+    constexpr int T = KT<LOGN>;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            uint32_t w[8];
+            tmem_ld8(ta + 32 * c + 8 * q, w);
+            u64 *o = c ? o1 : o0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int i = 2 * q + h;
+                u64 r0, r1;
+                if constexpr (FP) {
+                    r0 = ntt::fcanon(__hiloint2double(w[4 * h + 1], w[4 * h]), P.pd, P.pinvd);
+                    r1 = ntt::fcanon(__hiloint2double(w[4 * h + 3], w[4 * h + 2]), P.pd, P.pinvd);
+                } else {
+                    r0 = csub((u64)w[4 * h + 1] << 32 | w[4 * h], P.p);
+                    r1 = csub((u64)w[4 * h + 3] << 32 | w[4 * h + 2], P.p);
+                }
+                __stcg(reinterpret_cast<ulonglong2 *>(o + pos + 2 * T * i), make_ulonglong2(r0, r1));
+            }
+        }
+    }
+}
+
+template <int LOGN>
+__global__ void ROW_BOUNDS(LOGN) k_ks_modup_fused(Ctx K, heb_ct src, int comp, const i64 *D, const ulonglong2 *key,
+                                                  int k, u64 *acc, int64_t count) {
+    extern __shared__ u64 sm[];
+    __shared__ uint32_t tbase;
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&tbase))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t ta = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+
+    // targets in an interleaved order: the two wide (integer) targets 0 and k are spread
+    // between the narrow ones so co-resident CTAs mix IMAD- and DFMA-bound work
+    const int xi = lbx<LOGN>();
+    const int t = xi == 0 ? 0 : (xi == (k + 1) / 2 ? k : (xi < (k + 1) / 2 ? xi : xi - 1));
+    const int gt = t < k ? t : K.num_rows - 1;
+    const PrimeInfo P = K.pi[gt];
+    const int n = 1 << LOGN, R = K.num_rows;
+    const int pos = tpos<LOGN>();
+    for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
+        bool first = true;
+        for (int j = 0; j < k; ++j) {
+            u64 y[16];
+            if (j == t) {
+                load16<LOGN>(at(src, b, comp, t, LOGN) + pos, y);  // d2_t: congruent digit, no transform
+            } else {
+                const i64 *dj = D + (b * k + j) * n;
+                fwd_any<LOGN>(K, gt, P, sm,
+                              [&](int i) { return signed_mul_const(__ldcg(dj + i), P.rmod, P.rmod_s, P.p); }, y);
+            }
+            const ulonglong2 *keyrow = key + (((size_t)j * R + gt) * 2) * n;
+            if (HEB_FPSEL(P.use_fp))
+                modup_acc<LOGN, true>(ta, y, keyrow, pos, first, P);
+            else
+                modup_acc<LOGN, false>(ta, y, keyrow, pos, first, P);
+            first = false;
+        }
+        u64 *o0 = acc + ((b * 2 + 0) * (k + 1) + t) * n;
+        u64 *o1 = acc + ((b * 2 + 1) * (k + 1) + t) * n;
+        if (HEB_FPSEL(P.use_fp))
+            modup_store<LOGN, true>(ta, o0, o1, pos, P);
+        else
+            modup_store<LOGN, false>(ta, o0, o1, pos, P);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tbase) : "memory");
+}
+
 // acc[item][c][t][x] = sum_j v_j[x] * key_c[j][gt][x]  (Shoup with the prepared key)
 // Each thread owns two adjacent positions (16-byte accesses) and issues the loads of
 // MJ digits before using them, so every thread keeps MJ HBM reads in flight -- the
@@ -464,6 +622,7 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
     constexpr size_t sm = smem_bytes<LOGN>();
     CUDA_TRY(prep_kernel(k_ks_head<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_ks_modup_ntt<LOGN>, sm));
+    CUDA_TRY(prep_kernel(k_ks_modup_fused<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_ks_down_head<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_ks_down_head_cl<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_ks_down_rescale_tail<LOGN>, sm));
@@ -477,12 +636,20 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
         return e ? std::max<int64_t>(64, atoll(e)) : (int64_t)2400;
     }();
     const int64_t sub = std::max<int64_t>(4, std::min<int64_t>(cmax, (target_ctas + k * k - 1) / (k * k)));
+    // ModUp: TMEM-accumulating fused kernel by default (HEB_MODUP_SPLIT=1: the two-pass
+    // NTT + MAC path with the V intermediate in HBM)
+    static const bool fused_env = [] {
+        const char *e = getenv("HEB_MODUP_SPLIT");
+        return !(e && *e && *e != '0');
+    }();
+    // TMEM accesses are warp-wide: rows of fewer than 32 x 16 residues per CTA take the split path
+    const bool fused = fused_env && KT<LOGN> % 32 == 0;
     Scratch sD(c, st), sA(c, st), sP(c, st), sL(c, st), sV(c, st);
     CUDA_TRY(sD.get(sizeof(i64) * (size_t)cmax * k * n));
     CUDA_TRY(sA.get(sizeof(u64) * (size_t)cmax * 2 * (k + 1) * n));
     CUDA_TRY(sP.get(sizeof(i64) * (size_t)cmax * 2 * n));
     CUDA_TRY(sL.get(sizeof(u64) * (size_t)cmax * 2 * n));
-    CUDA_TRY(sV.get(sizeof(u64) * (size_t)sub * (k + 1) * k * n));
+    CUDA_TRY(sV.get(fused ? 256 : sizeof(u64) * (size_t)sub * (k + 1) * k * n));
     const Ctx K = kctx(c);
     for (int64_t b0 = 0; b0 < count; b0 += chunk) {
         const int64_t cnt = std::min<int64_t>(chunk, count - b0);
@@ -493,7 +660,12 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
         const unsigned gy = gdim(cnt);
         { PROF("k_ks_head", st, 16.0 * n * cnt * k); CUDA_TRY(launch_rows<LOGN>(k_ks_head<LOGN>, dim3(dim3(k, gy)), KT<LOGN>, sm, st, K, s, comp, (i64 *)sD.p, k, cnt)); }
         LAUNCH_CHECK();
-        for (int64_t s0 = 0; s0 < cnt; s0 += sub) {
+        if (fused) {
+            PROF("k_ks_modup_fused", st, 8.0 * n * cnt * ((double)k + 4.0 * k * (k + 1) / cnt + 2.0 * (k + 1)));
+            CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN>, dim3(dim3(k + 1, gy)), KT<LOGN>, sm, st, K, s, comp,
+                                       (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt));
+        }
+        for (int64_t s0 = 0; s0 < (fused ? 0 : cnt); s0 += sub) {
             const int64_t sc = std::min<int64_t>(sub, cnt - s0);
             heb_ct ss = s;
             ss.data += s0 * s.ct_stride;
