@@ -272,12 +272,18 @@ __device__ __forceinline__ void modup_store(uint32_t ta, u64 *o0, u64 *o1, int p
     }
 }
 
-template <int LOGN>
+// ENG: 0 = both engines in one launch, 1 = FP64-engine targets only, 2 = integer targets only
+template <int LOGN, int ENG>
 __global__ void ROW_BOUNDS(LOGN) k_ks_modup_fused(Ctx K, heb_ct src, int comp, const i64 *D, const ulonglong2 *key,
                                                   int k, u64 *acc, int64_t count) {
     extern __shared__ u64 sm[];
     __shared__ uint32_t tbase;
     const int warp = threadIdx.x >> 5;
+    if (ENG != 0) {
+        const int xi0 = lbx<LOGN>();
+        const int t0 = xi0 == 0 ? 0 : (xi0 == (k + 1) / 2 ? k : (xi0 < (k + 1) / 2 ? xi0 : xi0 - 1));
+        if (K.pi[t0 < k ? t0 : K.num_rows - 1].use_fp != (ENG == 1)) return;
+    }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
                          (uint32_t)__cvta_generic_to_shared(&tbase))
@@ -305,11 +311,27 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_modup_fused(Ctx K, heb_ct src, int comp, c
                 load16<LOGN>(at(src, b, comp, t, LOGN) + pos, y);  // d2_t: congruent digit, no transform
             } else {
                 const i64 *dj = D + (b * k + j) * n;
-                fwd_any<LOGN>(K, gt, P, sm,
-                              [&](int i) { return signed_mul_const(__ldcg(dj + i), P.rmod, P.rmod_s, P.p); }, y);
+                auto ld = [&](int i) { return signed_mul_const(__ldcg(dj + i), P.rmod, P.rmod_s, P.p); };
+                if constexpr (ENG == 0) {
+                    fwd_any<LOGN>(K, gt, P, sm, ld, y);
+                } else {
+                    constexpr int LL = Row<LOGN>::LL;
+                    if constexpr (ENG == 1) {
+                        const ntt::FpArith ar(P.pd, P.pinvd);
+                        double *s2 = reinterpret_cast<double *>(sm);
+                        const double *tw = K.twf + ((size_t)gt << LOGN);
+                        if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, 16>(ar, s2, tw, ld, y, rhalf<LOGN>());
+                        else ntt::forward<LL, 16>(ar, s2, tw, ld, y);
+                    } else {
+                        const ntt::IntArith ar(P.p);
+                        const ulonglong2 *tw = K.tw + ((size_t)gt << LOGN);
+                        if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, 16>(ar, sm, tw, ld, y, rhalf<LOGN>());
+                        else ntt::forward<LL, 16>(ar, sm, tw, ld, y);
+                    }
+                }
             }
             const ulonglong2 *keyrow = key + (((size_t)j * R + gt) * 2) * n;
-            if (HEB_FPSEL(P.use_fp))
+            if (ENG == 1 || (ENG == 0 && HEB_FPSEL(P.use_fp)))
                 modup_acc<LOGN, true>(ta, y, keyrow, pos, first, P);
             else
                 modup_acc<LOGN, false>(ta, y, keyrow, pos, first, P);
@@ -317,7 +339,7 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_modup_fused(Ctx K, heb_ct src, int comp, c
         }
         u64 *o0 = acc + ((b * 2 + 0) * (k + 1) + t) * n;
         u64 *o1 = acc + ((b * 2 + 1) * (k + 1) + t) * n;
-        if (HEB_FPSEL(P.use_fp))
+        if (ENG == 1 || (ENG == 0 && HEB_FPSEL(P.use_fp)))
             modup_store<LOGN, true>(ta, o0, o1, pos, P);
         else
             modup_store<LOGN, false>(ta, o0, o1, pos, P);
@@ -622,7 +644,9 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
     constexpr size_t sm = smem_bytes<LOGN>();
     CUDA_TRY(prep_kernel(k_ks_head<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_ks_modup_ntt<LOGN>, sm));
-    CUDA_TRY(prep_kernel(k_ks_modup_fused<LOGN>, sm));
+    CUDA_TRY(prep_kernel(k_ks_modup_fused<LOGN, 0>, sm));
+    CUDA_TRY(prep_kernel(k_ks_modup_fused<LOGN, 1>, sm));
+    CUDA_TRY(prep_kernel(k_ks_modup_fused<LOGN, 2>, sm));
     CUDA_TRY(prep_kernel(k_ks_down_head<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_ks_down_head_cl<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_ks_down_rescale_tail<LOGN>, sm));
@@ -662,8 +686,18 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
         LAUNCH_CHECK();
         if (fused) {
             PROF("k_ks_modup_fused", st, 8.0 * n * cnt * ((double)k + 4.0 * k * (k + 1) / cnt + 2.0 * (k + 1)));
-            CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN>, dim3(dim3(k + 1, gy)), KT<LOGN>, sm, st, K, s, comp,
-                                       (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt));
+#ifndef MODUP_ENGINES_SPLIT
+#define MODUP_ENGINES_SPLIT 1
+#endif
+            if (MODUP_ENGINES_SPLIT) {
+                CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 2>, dim3(dim3(k + 1, gy)), KT<LOGN>, sm, st, K, s,
+                                           comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt));
+                CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 1>, dim3(dim3(k + 1, gy)), KT<LOGN>, sm, st, K, s,
+                                           comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt));
+            } else {
+                CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 0>, dim3(dim3(k + 1, gy)), KT<LOGN>, sm, st, K, s,
+                                           comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt));
+            }
         }
         for (int64_t s0 = 0; s0 < (fused ? 0 : cnt); s0 += sub) {
             const int64_t sc = std::min<int64_t>(sub, cnt - s0);
