@@ -82,6 +82,7 @@ struct StreamArena {
 struct heb_ctx {
     int device = 0, log_n = 0, n = 0, num_rows = 0, chunk = 1024;
     std::vector<u64> primes;
+    std::vector<char> row_fp;  // host copy of PrimeInfo::use_fp per chain row
     PrimeInfo *d_pi = nullptr;
     ulonglong2 *d_tw = nullptr, *d_itw = nullptr;
     double *d_twf = nullptr, *d_itwf = nullptr;  // FP64 engine twiddles (w as double)
@@ -201,17 +202,37 @@ __device__ __forceinline__ int tpos() {
 // Row-dispatched transforms: rows whose prime is < 2^42 run on the FP64 engine, the
 // others (50/60-bit base and special primes) on the 64-bit integer engine.  Both read
 // u64 residues and return canonical u64 residues, so callers are engine-agnostic.
-template <int LOGN, int E = 16, class Load>
+// ENG (kernels instantiated per engine): 0 = dispatch on the row at run time, 1 = FP64
+// engine only, 2 = integer engine only.  One instantiation per engine is register-
+// allocated on its own (no spills carried over from the other engine's code).
+template <int ENG>
+__device__ __forceinline__ bool eng_fp(const PrimeInfo &P) {
+    if constexpr (ENG == 1) return true;
+    else if constexpr (ENG == 2) return false;
+    else return HEB_FPSEL(P.use_fp);
+}
+template <int ENG>
+__device__ __forceinline__ bool eng_skip(const PrimeInfo &P) {  // row belongs to the other instantiation
+    return ENG != 0 && (bool)P.use_fp != (ENG == 1);
+}
+template <int LOGN, int E = 16, int ENG = 0, class Load>
 __device__ __forceinline__ void fwd_any(const Ctx &K, int row, const PrimeInfo &P, u64 *sm, Load load,
                                         u64 (&out)[E]) {
     constexpr int LL = Row<LOGN>::LL;
-    if (HEB_FPSEL(P.use_fp)) {
+    if constexpr (ENG == 2) {
+        const ntt::IntArith ar(P.p);
+        const ulonglong2 *tw = K.tw + ((size_t)row << LOGN);
+        if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, E>(ar, sm, tw, load, out, rhalf<LOGN>());
+        else ntt::forward<LL, E>(ar, sm, tw, load, out);
+        return;
+    }
+    if (ENG == 1 || HEB_FPSEL(P.use_fp)) {
         const ntt::FpArith ar(P.pd, P.pinvd);
         double *s = reinterpret_cast<double *>(sm);
         const double *tw = K.twf + ((size_t)row << LOGN);
         if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, E>(ar, s, tw, load, out, rhalf<LOGN>());
         else ntt::forward<LL, E>(ar, s, tw, load, out);
-    } else {
+    } else if constexpr (ENG == 0) {
         const ntt::IntArith ar(P.p);
         const ulonglong2 *tw = K.tw + ((size_t)row << LOGN);
         if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, E>(ar, sm, tw, load, out, rhalf<LOGN>());
@@ -219,19 +240,27 @@ __device__ __forceinline__ void fwd_any(const Ctx &K, int row, const PrimeInfo &
     }
 }
 // std_out: fold the from-Montgomery factor R^-1 into the final stage
-template <int LOGN, int E = 16, class Store>
+template <int LOGN, int E = 16, int ENG = 0, class Store>
 __device__ __forceinline__ void inv_any(const Ctx &K, int row, const PrimeInfo &P, u64 *sm, const u64 (&in)[E],
                                         Store store, bool std_out) {
     constexpr int LL = Row<LOGN>::LL;
     const LastConst &lc = K.last[row];
-    if (HEB_FPSEL(P.use_fp)) {
+    if constexpr (ENG == 2) {
+        const ntt::IntArith ar(P.p);
+        const ulonglong2 *itw = K.itw + ((size_t)row << LOGN);
+        const ulonglong2 u = std_out ? lc.u_std : lc.u_plain, v = std_out ? lc.v_std : lc.v_plain;
+        if constexpr (Row<LOGN>::SPLIT) ntt::inverse_split<LL, E>(ar, sm, itw, in, store, u, v, rhalf<LOGN>());
+        else ntt::inverse<LL, E>(ar, sm, itw, in, store, u, v);
+        return;
+    }
+    if (ENG == 1 || HEB_FPSEL(P.use_fp)) {
         const ntt::FpArith ar(P.pd, P.pinvd);
         double *s = reinterpret_cast<double *>(sm);
         const double *itw = K.itwf + ((size_t)row << LOGN);
         const double u = std_out ? lc.fu_std : lc.fu_plain, v = std_out ? lc.fv_std : lc.fv_plain;
         if constexpr (Row<LOGN>::SPLIT) ntt::inverse_split<LL, E>(ar, s, itw, in, store, u, v, rhalf<LOGN>());
         else ntt::inverse<LL, E>(ar, s, itw, in, store, u, v);
-    } else {
+    } else if constexpr (ENG == 0) {
         const ntt::IntArith ar(P.p);
         const ulonglong2 *itw = K.itw + ((size_t)row << LOGN);
         const ulonglong2 u = std_out ? lc.u_std : lc.u_plain, v = std_out ? lc.v_std : lc.v_plain;
@@ -263,6 +292,36 @@ static cudaError_t launch_rows(Kern kernel, dim3 grid, int block, size_t smem, c
         return cudaGetLastError();
     }
 }
+
+// Launch a row kernel over chain rows [a, b) (its blockIdx.x row = r0 + lbx, r0 passed
+// as the kernel's last argument).  When the integer-engine rows form a prefix of the
+// range (the usual chain layout: wide base prime first, 40-bit level primes after) the
+// rows are split over the integer-only and FP64-only instantiations, each register-
+// allocated on its own; otherwise the run-time dispatching instantiation covers all.
+template <int LOGN, class K0, class K1, class K2, class... Args>
+static cudaError_t launch_by_engine(const heb_ctx *c, K0 k0, K1 k1, K2 k2, int a, int b, unsigned gy, unsigned gz,
+                                    size_t smem, cudaStream_t st, Args... args) {
+    if (b <= a) return cudaSuccess;
+#ifndef ENGINE_SPLIT_ROWS
+#define ENGINE_SPLIT_ROWS 0  // measured: the small integer-row launch runs alone and loses more than it saves
+#endif
+    if (!ENGINE_SPLIT_ROWS) return launch_rows<LOGN>(k0, dim3(b - a, gy, gz), KT<LOGN>, smem, st, args..., a);
+    int nint = 0;
+    while (a + nint < b && !c->row_fp[a + nint]) ++nint;
+    bool rest_fp = true;
+    for (int r = a + nint; r < b; ++r) rest_fp = rest_fp && c->row_fp[r];
+    if (!rest_fp) return launch_rows<LOGN>(k0, dim3(b - a, gy, gz), KT<LOGN>, smem, st, args..., a);
+    cudaError_t e = cudaSuccess;
+    if (nint) e = launch_rows<LOGN>(k2, dim3(nint, gy, gz), KT<LOGN>, smem, st, args..., a);
+    if (e == cudaSuccess && b - a - nint)
+        e = launch_rows<LOGN>(k1, dim3(b - a - nint, gy, gz), KT<LOGN>, smem, st, args..., a + nint);
+    return e;
+}
+#define ENGINE_KERNELS(KERN) KERN<LOGN, 0>, KERN<LOGN, 1>, KERN<LOGN, 2>
+#define PREP_ENGINES(KERN, SM)                       \
+    CUDA_TRY(prep_kernel(KERN<LOGN, 0>, SM));        \
+    CUDA_TRY(prep_kernel(KERN<LOGN, 1>, SM));        \
+    CUDA_TRY(prep_kernel(KERN<LOGN, 2>, SM))
 
 template <int LOGN>
 __device__ __forceinline__ const ulonglong2 *tw_row(const Ctx &k, int row) {

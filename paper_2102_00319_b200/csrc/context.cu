@@ -131,6 +131,7 @@ extern "C" int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows
         q.pd = (double)p;
         q.pinvd = 1.0 / (double)p;
         q.use_fp = (p < (1ull << 42)) && !fp_disabled;
+        c->row_fp.push_back(q.use_fp ? 1 : 0);
         auto fpair = [&](u64 w) { return (double)w; };
         for (int i = 0; i < n; ++i) {
             twf[(size_t)r * n + i] = fpair(tw[(size_t)r * n + i].x);

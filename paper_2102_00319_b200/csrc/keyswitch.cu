@@ -6,7 +6,7 @@
 //   head: v = center(INTT_L(c_L [* pt_L]))                      (1 INTT / component)
 //   tail: out_i = c_i [* pt_i] * qL^-1 - NTT_i(v * qL^-1 * R)  (k-1 NTTs / component)
 // =============================================================================
-template <int LOGN>
+template <int LOGN, int ENG>
 __global__ void ROW_BOUNDS(LOGN) k_rescale_head(Ctx K, heb_ct in, const u64 *pt,
                                                                         int64_t pstride, i64 *V, int comps, int L,
                                                                         int64_t count) {
@@ -24,22 +24,22 @@ __global__ void ROW_BOUNDS(LOGN) k_rescale_head(Ctx K, heb_ct in, const u64 *pt,
             for (int m = 0; m < 16; ++m) x[m] = mont_mul(x[m], y[m], P.p, P.pinv);
         }
         i64 *dst = V + (b * comps + c) * (1 << LOGN);
-        inv_any<LOGN>(K, L, P, sm, x, [&](int i, u64 v) { dst[i] = center(v, P.p); }, true);
+        inv_any<LOGN, 16, ENG>(K, L, P, sm, x, [&](int i, u64 v) { dst[i] = center(v, P.p); }, true);
     }
 }
 
-template <int LOGN>
+template <int LOGN, int ENG>
 __global__ void ROW_BOUNDS(LOGN) k_rescale_tail(Ctx K, heb_ct in, const u64 *pt,
                                                                         int64_t pstride, const i64 *V, heb_ct out,
-                                                                        int comps, int L, int64_t count) {
+                                                                        int comps, int L, int64_t count, int r0) {
     extern __shared__ u64 sm[];
-    const int i = lbx<LOGN>(), c = blockIdx.z;
+    const int i = r0 + lbx<LOGN>(), c = blockIdx.z;
     const PrimeInfo P = K.pi[i];
     const LevelConst C = K.lc[(size_t)L * K.num_rows + i];
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         const i64 *src = V + (b * comps + c) * (1 << LOGN);
         u64 y[16];
-        fwd_any<LOGN>(K, i, P, sm,
+        fwd_any<LOGN, 16, ENG>(K, i, P, sm,
                            [&](int j) { return signed_mul_const(__ldcg(src + j), C.beta_r.x, C.beta_r.y, P.p); }, y);
         u64 x[16];
         load16<LOGN>(at(in, b, c, i, LOGN) + tpos<LOGN>(), x);
@@ -60,8 +60,8 @@ static int launch_rescale(heb_ctx *c, heb_ct in, const u64 *pt, int64_t pstride,
                           int level, cudaStream_t st) {
     constexpr int T = KT<LOGN>;
     constexpr size_t sm = smem_bytes<LOGN>();
-    CUDA_TRY(prep_kernel(k_rescale_head<LOGN>, sm));
-    CUDA_TRY(prep_kernel(k_rescale_tail<LOGN>, sm));
+    PREP_ENGINES(k_rescale_head, sm);
+    PREP_ENGINES(k_rescale_tail, sm);
     const int64_t chunk = c->chunk > 0 ? c->chunk * 4 : count;
     Scratch V(c, st);
     CUDA_TRY(V.get(sizeof(i64) * (size_t)std::min<int64_t>(count, chunk) * comps * c->n));
@@ -71,10 +71,10 @@ static int launch_rescale(heb_ctx *c, heb_ct in, const u64 *pt, int64_t pstride,
         ib.data += b0 * in.ct_stride;
         ob.data += b0 * out.ct_stride;
         const u64 *pb = pt ? pt + b0 * pstride : nullptr;
-        { PROF("k_rescale_head", st, 8.0 * c->n * (2.0 * cnt * comps + (pt ? (pstride ? cnt : 1) : 0))); CUDA_TRY(launch_rows<LOGN>(k_rescale_head<LOGN>, dim3(dim3(comps, gdim(cnt))), KT<LOGN>, sm, st, kctx(c), ib, pb, pstride, (i64 *)V.p, comps,
+        { PROF("k_rescale_head", st, 8.0 * c->n * (2.0 * cnt * comps + (pt ? (pstride ? cnt : 1) : 0))); CUDA_TRY(launch_rows<LOGN>(c->row_fp[level] ? k_rescale_head<LOGN, 1> : k_rescale_head<LOGN, 2>, dim3(dim3(comps, gdim(cnt))), KT<LOGN>, sm, st, kctx(c), ib, pb, pstride, (i64 *)V.p, comps,
                                                                      level, cnt)); }
         LAUNCH_CHECK();
-        { PROF("k_rescale_tail", st, 8.0 * c->n * (cnt * comps * (1.0 + 2.0 * level) + (pt ? level * (pstride ? cnt : 1) : 0))); CUDA_TRY(launch_rows<LOGN>(k_rescale_tail<LOGN>, dim3(dim3(level, gdim(cnt), comps)), KT<LOGN>, sm, st, kctx(c), ib, pb, pstride,
+        { PROF("k_rescale_tail", st, 8.0 * c->n * (cnt * comps * (1.0 + 2.0 * level) + (pt ? level * (pstride ? cnt : 1) : 0))); CUDA_TRY(launch_by_engine<LOGN>(c, ENGINE_KERNELS(k_rescale_tail), 0, level, gdim(cnt), comps, sm, st, kctx(c), ib, pb, pstride,
                                                                             (const i64 *)V.p, ob, comps, level, cnt)); }
         LAUNCH_CHECK();
     }
@@ -102,18 +102,18 @@ extern "C" int heb_rescale(heb_ctx *c, heb_ct in, const uint64_t *pt, int64_t ps
 // which equals moddown -> add d -> divide_drop_last of the reference exactly,
 // since every step is an identity mod q_i.
 // =============================================================================
-template <int LOGN>
+template <int LOGN, int ENG>
 __global__ void ROW_BOUNDS(LOGN) k_ks_head(Ctx K, heb_ct src, int comp, i64 *D, int k,
-                                                                   int64_t count) {
+                                                                   int64_t count, int r0) {
     extern __shared__ u64 sm[];
-    const int j = lbx<LOGN>();
+    const int j = r0 + lbx<LOGN>();
     const PrimeInfo P = K.pi[j];
     const LastConst lc = K.last[j];
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         u64 x[16];
         load16<LOGN>(at(src, b, comp, j, LOGN) + tpos<LOGN>(), x);
         i64 *dst = D + (b * k + j) * (1 << LOGN);
-        inv_any<LOGN>(K, j, P, sm, x, [&](int i, u64 v) { dst[i] = center(v, P.p); }, true);
+        inv_any<LOGN, 16, ENG>(K, j, P, sm, x, [&](int i, u64 v) { dst[i] = center(v, P.p); }, true);
     }
 }
 
@@ -477,7 +477,7 @@ extern "C" int heb_prepare_switch_key(heb_ctx *c, const uint64_t *kb, const uint
 }
 
 // which = 0: aP = center_P(INTT_P(acc_P)) ; which = 1: bL = INTT_L(acc_L + P d_L) (std form)
-template <int LOGN>
+template <int LOGN, int ENG>
 __global__ void ROW_BOUNDS(LOGN) k_ks_down_head(Ctx K, const u64 *acc, heb_ct d, int k,
                                                                         i64 *aP, u64 *bL, int64_t count) {
     extern __shared__ u64 sm[];
@@ -498,10 +498,10 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_down_head(Ctx K, const u64 *acc, heb_ct d,
 #pragma unroll
             for (int m = 0; m < 16; ++m) x[m] = add_mod(x[m], shoup(y[m], C.pmod.x, C.pmod.y, P.p), P.p);
             u64 *dst = bL + (b * 2 + c) * n;
-            inv_any<LOGN>(K, row, P, sm, x, [&](int i, u64 v) { dst[i] = v; }, true);
+            inv_any<LOGN, 16, ENG>(K, row, P, sm, x, [&](int i, u64 v) { dst[i] = v; }, true);
         } else {
             i64 *dst = aP + (b * 2 + c) * n;
-            inv_any<LOGN>(K, row, P, sm, x, [&](int i, u64 v) { dst[i] = center(v, P.p); }, true);
+            inv_any<LOGN, 16, ENG>(K, row, P, sm, x, [&](int i, u64 v) { dst[i] = center(v, P.p); }, true);
         }
     }
 }
@@ -518,7 +518,7 @@ __device__ __forceinline__ double fp_imul(i64 a, double w, double w32, double pd
 //   cL = center((INTT_L(acc_L + P d_L) - aP) P^-1 mod q_L)
 // cL depends only on (item, component, position); computing it here once (instead of
 // in each of the k-1 tail rows) removes most of the tail's integer prologue.
-template <int LOGN>
+template <int LOGN, int ENG>
 __global__ void ROW_BOUNDS(LOGN) k_ks_down_head_cl(Ctx K, const u64 *acc, heb_ct d, int k, const i64 *aP, i64 *cL,
                                                    int64_t count) {
     extern __shared__ u64 sm[];
@@ -536,7 +536,7 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_down_head_cl(Ctx K, const u64 *acc, heb_ct
         load16<LOGN>(at(d, b, c, L, LOGN) + pos, y);
 #pragma unroll
         for (int m = 0; m < 16; ++m) x[m] = add_mod(x[m], shoup(y[m], C.pmod.x, C.pmod.y, PL.p), PL.p);
-        inv_any<LOGN>(K, L, PL, sm, x,
+        inv_any<LOGN, 16, ENG>(K, L, PL, sm, x,
                       [&](int i, u64 v) {
                           const u64 sl = sub_mod(shoup(v, C.pinv.x, C.pinv.y, PL.p),
                                                  signed_mul_const(__ldcg(ap + i), C.pinv.x, C.pinv.y, PL.p), PL.p);
@@ -546,17 +546,17 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_down_head_cl(Ctx K, const u64 *acc, heb_ct
     }
 }
 
-template <int LOGN>
+template <int LOGN, int ENG>
 __global__ void ROW_BOUNDS(LOGN) k_ks_down_rescale_tail(Ctx K, const u64 *acc, heb_ct d, const i64 *aP, const i64 *cL,
-                                                        int k, heb_ct out, int64_t count) {
+                                                        int k, heb_ct out, int64_t count, int r0) {
     extern __shared__ u64 sm[];
-    const int i = lbx<LOGN>(), c = blockIdx.z;
+    const int i = r0 + lbx<LOGN>(), c = blockIdx.z;
     const int n = 1 << LOGN;
     const int pos = tpos<LOGN>();
     const int L = k - 1;
     const PrimeInfo Pi = K.pi[i];
     const LevelConst Ci = K.lc[(size_t)L * K.num_rows + i];  // level L: drop q_L
-    if (HEB_FPSEL(Pi.use_fp)) {
+    if (eng_fp<ENG>(Pi)) {
         // FP64 row: every product is an exact FP64 modular product (the integer pipe is
         // this kernel's bottleneck otherwise)
         const double pd = Pi.pd, pinvd = Pi.pinvd;
@@ -567,7 +567,7 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_down_rescale_tail(Ctx K, const u64 *acc, h
             const i64 *ap = aP + (b * 2 + c) * n;
             const i64 *cl = cL + (b * 2 + c) * n;
             u64 y[16];
-            fwd_any<LOGN>(K, i, Pi, sm,
+            fwd_any<LOGN, 16, ENG>(K, i, Pi, sm,
                           [&](int j) {
                               const double v = fp_imul(__ldcg(ap + j), ar, ar32, pd, pinvd) +
                                                ntt::fmul((double)__ldcg(cl + j), br, pd, pinvd);
@@ -590,7 +590,7 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_down_rescale_tail(Ctx K, const u64 *acc, h
         const i64 *ap = aP + (b * 2 + c) * n;
         const i64 *cl = cL + (b * 2 + c) * n;
         u64 y[16];
-        fwd_any<LOGN>(K, i, Pi, sm,
+        fwd_any<LOGN, 16, ENG>(K, i, Pi, sm,
             [&](int j) {
                 return add_mod(signed_mul_const(__ldcg(ap + j), Ci.alpha_r.x, Ci.alpha_r.y, Pi.p),
                                signed_mul_const(__ldcg(cl + j), Ci.beta_r.x, Ci.beta_r.y, Pi.p), Pi.p);
@@ -609,11 +609,11 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_down_rescale_tail(Ctx K, const u64 *acc, h
 }
 
 // ModDown without rescale (rotation): out_i = acc_i P^-1 - NTT_i(aP P^-1 R) [+ add0_i for c = 0]
-template <int LOGN>
+template <int LOGN, int ENG>
 __global__ void ROW_BOUNDS(LOGN) k_ks_down_tail(Ctx K, const u64 *acc, const i64 *aP, int k,
-                                                                        heb_ct add0, heb_ct out, int64_t count) {
+                                                                        heb_ct add0, heb_ct out, int64_t count, int r0) {
     extern __shared__ u64 sm[];
-    const int i = lbx<LOGN>(), c = blockIdx.z;
+    const int i = r0 + lbx<LOGN>(), c = blockIdx.z;
     const int n = 1 << LOGN;
     const int pos = tpos<LOGN>();
     const PrimeInfo Pi = K.pi[i];
@@ -621,7 +621,7 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_down_tail(Ctx K, const u64 *acc, const i64
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         const i64 *ap = aP + (b * 2 + c) * n;
         u64 y[16];
-        fwd_any<LOGN>(K, i, Pi, sm,
+        fwd_any<LOGN, 16, ENG>(K, i, Pi, sm,
                            [&](int j) { return signed_mul_const(__ldcg(ap + j), Ci.gamma_r.x, Ci.gamma_r.y, Pi.p); }, y);
         u64 x[16];
         load16<LOGN>(acc + ((b * 2 + c) * (k + 1) + i) * n + pos, x);
@@ -642,15 +642,15 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
                             int64_t count, int level, bool rescale, cudaStream_t st) {
     constexpr int T = KT<LOGN>;
     constexpr size_t sm = smem_bytes<LOGN>();
-    CUDA_TRY(prep_kernel(k_ks_head<LOGN>, sm));
+    PREP_ENGINES(k_ks_head, sm);
     CUDA_TRY(prep_kernel(k_ks_modup_ntt<LOGN>, sm));
     CUDA_TRY(prep_kernel(k_ks_modup_fused<LOGN, 0>, sm));
     CUDA_TRY(prep_kernel(k_ks_modup_fused<LOGN, 1>, sm));
     CUDA_TRY(prep_kernel(k_ks_modup_fused<LOGN, 2>, sm));
-    CUDA_TRY(prep_kernel(k_ks_down_head<LOGN>, sm));
-    CUDA_TRY(prep_kernel(k_ks_down_head_cl<LOGN>, sm));
-    CUDA_TRY(prep_kernel(k_ks_down_rescale_tail<LOGN>, sm));
-    CUDA_TRY(prep_kernel(k_ks_down_tail<LOGN>, sm));
+    PREP_ENGINES(k_ks_down_head, sm);
+    PREP_ENGINES(k_ks_down_head_cl, sm);
+    PREP_ENGINES(k_ks_down_rescale_tail, sm);
+    PREP_ENGINES(k_ks_down_tail, sm);
     const int k = level + 1, n = c->n;
     const int64_t chunk = c->chunk > 0 ? c->chunk : count;
     const int64_t cmax = std::min<int64_t>(chunk, count);
@@ -682,7 +682,7 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
         dd.data += b0 * d.ct_stride;
         o.data += b0 * out.ct_stride;
         const unsigned gy = gdim(cnt);
-        { PROF("k_ks_head", st, 16.0 * n * cnt * k); CUDA_TRY(launch_rows<LOGN>(k_ks_head<LOGN>, dim3(dim3(k, gy)), KT<LOGN>, sm, st, K, s, comp, (i64 *)sD.p, k, cnt)); }
+        { PROF("k_ks_head", st, 16.0 * n * cnt * k); CUDA_TRY(launch_by_engine<LOGN>(c, ENGINE_KERNELS(k_ks_head), 0, k, gy, 1, sm, st, K, s, comp, (i64 *)sD.p, k, cnt)); }
         LAUNCH_CHECK();
         if (fused) {
             PROF("k_ks_modup_fused", st, 8.0 * n * cnt * ((double)k + 4.0 * k * (k + 1) / cnt + 2.0 * (k + 1)));
@@ -719,21 +719,21 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
             LAUNCH_CHECK();
         }
         if (rescale) {
-            { PROF("k_ks_down_head", st, 8.0 * n * cnt * 4.0); CUDA_TRY(launch_rows<LOGN>(k_ks_down_head<LOGN>, dim3(dim3(1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
+            { PROF("k_ks_down_head", st, 8.0 * n * cnt * 4.0); CUDA_TRY(launch_rows<LOGN>(c->row_fp[c->num_rows - 1] ? k_ks_down_head<LOGN, 1> : k_ks_down_head<LOGN, 2>, dim3(dim3(1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
                                                                  (u64 *)nullptr, cnt)); }
             LAUNCH_CHECK();
-            { PROF("k_ks_down_head_cl", st, 8.0 * n * cnt * 2.0 * 4.0); CUDA_TRY(launch_rows<LOGN>(k_ks_down_head_cl<LOGN>, dim3(dim3(1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd, k, (const i64 *)sP.p,
+            { PROF("k_ks_down_head_cl", st, 8.0 * n * cnt * 2.0 * 4.0); CUDA_TRY(launch_rows<LOGN>(c->row_fp[k - 1] ? k_ks_down_head_cl<LOGN, 1> : k_ks_down_head_cl<LOGN, 2>, dim3(dim3(1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd, k, (const i64 *)sP.p,
                                                                  (i64 *)sL.p, cnt)); }
             LAUNCH_CHECK();
-            { PROF("k_ks_down_rescale_tail", st, 8.0 * n * cnt * 2.0 * (2 + 3 * (k - 1))); CUDA_TRY(launch_rows<LOGN>(k_ks_down_rescale_tail<LOGN>, dim3(dim3(k - 1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd,
+            { PROF("k_ks_down_rescale_tail", st, 8.0 * n * cnt * 2.0 * (2 + 3 * (k - 1))); CUDA_TRY(launch_by_engine<LOGN>(c, ENGINE_KERNELS(k_ks_down_rescale_tail), 0, k - 1, gy, 2, sm, st, K, (const u64 *)sA.p, dd,
                                                                              (const i64 *)sP.p, (const i64 *)sL.p, k,
                                                                              o, cnt)); }
             LAUNCH_CHECK();
         } else {
-            { PROF("k_ks_down_head", st, 8.0 * n * cnt * 4.0); CUDA_TRY(launch_rows<LOGN>(k_ks_down_head<LOGN>, dim3(dim3(1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
+            { PROF("k_ks_down_head", st, 8.0 * n * cnt * 4.0); CUDA_TRY(launch_rows<LOGN>(c->row_fp[c->num_rows - 1] ? k_ks_down_head<LOGN, 1> : k_ks_down_head<LOGN, 2>, dim3(dim3(1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
                                                                  (u64 *)sL.p, cnt)); }
             LAUNCH_CHECK();
-            { PROF("k_ks_down_tail", st, 8.0 * n * cnt * (2.0 + 5.0 * k)); CUDA_TRY(launch_rows<LOGN>(k_ks_down_tail<LOGN>, dim3(dim3(k, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, (const i64 *)sP.p, k, dd, o,
+            { PROF("k_ks_down_tail", st, 8.0 * n * cnt * (2.0 + 5.0 * k)); CUDA_TRY(launch_by_engine<LOGN>(c, ENGINE_KERNELS(k_ks_down_tail), 0, k, gy, 2, sm, st, K, (const u64 *)sA.p, (const i64 *)sP.p, k, dd, o,
                                                                  cnt)); }
             LAUNCH_CHECK();
         }
