@@ -272,9 +272,24 @@ __device__ __forceinline__ void modup_store(uint32_t ta, u64 *o0, u64 *o1, int p
     }
 }
 
+// TMEM columns a CTA of T threads addresses: 64 per group of four warps (one warp per
+// lane quadrant), at least 32, a power of two as tcgen05.alloc requires.  Sized to the
+// block so that as many CTAs as the NTT launch bounds make resident also fit the SM's
+// 512 columns (an over-sized request leaves co-resident CTAs blocked in the alloc).
+template <int T>
+__host__ __device__ constexpr uint32_t modup_tmem_cols() {
+    constexpr uint32_t c = 64u * (uint32_t)((T / 32 + 3) / 4);
+    return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
+}
+
 // ENG: 0 = both engines in one launch, 1 = FP64-engine targets only, 2 = integer targets only
+// integer-engine targets (60-bit rows) may trade residency for registers: the Shoup
+// butterflies need more than the 64 registers two 512-thread CTAs per SM leave
+#ifndef MODUP_INT_MINB
+#define MODUP_INT_MINB(LOGN) NTT_MINB(LOGN)
+#endif
 template <int LOGN, int ENG>
-__global__ void ROW_BOUNDS(LOGN) k_ks_modup_fused(Ctx K, heb_ct src, int comp, const i64 *D, const ulonglong2 *key,
+__global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : NTT_MINB(LOGN)) k_ks_modup_fused(Ctx K, heb_ct src, int comp, const i64 *D, const ulonglong2 *key,
                                                   int k, u64 *acc, int64_t count) {
     extern __shared__ u64 sm[];
     __shared__ uint32_t tbase;
@@ -285,8 +300,9 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_modup_fused(Ctx K, heb_ct src, int comp, c
         if (K.pi[t0 < k ? t0 : K.num_rows - 1].use_fp != (ENG == 1)) return;
     }
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(&tbase))
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&tbase)),
+                     "n"(modup_tmem_cols<KT<LOGN>>())
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -347,7 +363,9 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_modup_fused(Ctx K, heb_ct src, int comp, c
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tbase) : "memory");
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(modup_tmem_cols<KT<LOGN>>())
+                     : "memory");
 }
 
 // acc[item][c][t][x] = sum_j v_j[x] * key_c[j][gt][x]  (Shoup with the prepared key)
