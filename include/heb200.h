@@ -157,6 +157,34 @@ int heb_sum_gather(heb_ctx *ctx, heb_ct a, const int32_t *idx, int terms, heb_ct
 int heb_gather(heb_ctx *ctx, heb_ct a, const int32_t *idx, heb_ct out, int64_t n_out, int comps, int k,
                void *stream);
 
+/* --- layer entry points (one call per encrypted-CNN layer, layers.py:92-294) ---------
+ * Operands are batches at `level` (k = level+1 rows); outputs are written at the level
+ * the reference's layer returns.  Intermediates live in the stream's scratch arena.
+ * evk = prepared relinearisation key (heb_prepare_switch_key).  The host keeps the
+ * level / scale / noise ledger (base.py:354-502). */
+/* conv2d_enc (layers.py:92-127) for every output cell at once: raw = sum over the
+ * valid, strided window (heb_conv_tensor; index-driven heb_dot_tensor beyond its
+ * shared-memory stage), raw_finalize (relinearise + rescale), then bias[f] (bias.data
+ * NULL: none; else `filters` ciphertexts at >= the output level) added to filter f's
+ * cells.  out: filters*om*on ciphertexts at level-1, item f*om*on + i*on + j. */
+int heb_conv(heb_ctx *ctx, heb_ct x, heb_ct w, heb_ct bias, heb_ct out, int channels, int m, int n, int filters,
+             int kp, int kq, int stride, int level, const uint64_t *evk, void *stream);
+/* Standalone x^2 activation: mul_ct_ct(y, y) = tensor + raw_finalize (ckks.py:333-387). */
+int heb_square(heb_ctx *ctx, heb_ct y, heb_ct out, int64_t count, int level, const uint64_t *evk, void *stream);
+/* approx_relu_cell (layers.py:164-186) with the folded-coefficient plaintexts of
+ * _act_plaintexts (:139-161): out = (y^2 (*) pt_quad) + (y (*) pt_lin) + pt_const.
+ * pt_quad: level rows (k-1), pt_lin: k rows, pt_const: k-2 rows, each broadcast.
+ * out at level-2; level >= 2. */
+int heb_poly_act(heb_ctx *ctx, heb_ct y, const uint64_t *pt_quad, const uint64_t *pt_lin, const uint64_t *pt_const,
+                 heb_ct out, int64_t count, int level, const uint64_t *evk, void *stream);
+/* 2x2 sum pool of a channel-major map (channels, m, n) -> (channels, m/2, n/2):
+ * mean_pool_2x2's four-way add (layers.py:189-204) without the divisor. */
+int heb_sumpool(heb_ctx *ctx, heb_ct y, heb_ct out, int channels, int m, int n, int level, void *stream);
+/* dense_enc (layers.py:248-294): out_o = raw_finalize(sum_t X[x_idx[o*taps+t]] (x)
+ * W[w_idx[o*taps+t]]) + bias_o (bias.data NULL: none).  out at level-1. */
+int heb_fc(heb_ctx *ctx, heb_ct x, heb_ct w, const int32_t *x_idx, const int32_t *w_idx, int taps, heb_ct bias,
+           heb_ct out, int64_t n_out, int level, const uint64_t *evk, void *stream);
+
 /* --- transport (host <-> device wire format) --------------------------------------- */
 /* Residue rows bit-packed at bitlen(p_r) bits per residue: a block of rows 0..rows-1
  * takes heb_packed_words(rows) words (row r: ceil(N*bitlen(p_r)/64) words, in order);

@@ -63,6 +63,11 @@ SIGNATURES: dict[str, list] = {
     "heb_conv_tensor": [_P, _CT, _CT, _CT, _I, _I, _I, _I, _I, _I, _I, _I, _P],
     "heb_sum_gather": [_P, _CT, _P, _I, _CT, _L, _I, _I, _P],
     "heb_gather": [_P, _CT, _P, _CT, _L, _I, _I, _P],
+    "heb_conv": [_P, _CT, _CT, _CT, _CT, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P],
+    "heb_square": [_P, _CT, _CT, _L, _I, _P, _P],
+    "heb_poly_act": [_P, _CT, _P, _P, _P, _CT, _L, _I, _P, _P],
+    "heb_sumpool": [_P, _CT, _CT, _I, _I, _I, _I, _P],
+    "heb_fc": [_P, _CT, _CT, _P, _P, _I, _CT, _CT, _L, _I, _P, _P],
     "heb_packed_words": [_P, _I],
     "heb_pack_rows": [_P, _P, _L, _I, _L, _P, _P],
     "heb_unpack_rows": [_P, _P, _L, _I, _P, _L, _P],

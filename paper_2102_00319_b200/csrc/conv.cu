@@ -331,3 +331,7 @@ extern "C" int heb_conv_tensor(heb_ctx *c, heb_ct a, heb_ct b, heb_ct d, int cha
     LAUNCH_CHECK();
     return HEB_OK;
 }
+
+// Largest tap count heb_conv sends to the fused kernel: what its shared-memory stage
+// holds, capped at 64 (beyond that the index-driven heb_dot_tensor measured faster).
+int conv_tensor_max_taps() { return std::min(64, (int)(220 * 1024 / (sizeof(u64) * FG * 2 * XC))); }

@@ -5,13 +5,14 @@ The reference evaluates a layer as nested Python loops of per-ciphertext ops
 `executor.py:161-279` on a thread pool).  Here every layer is a handful of
 launches over *all* of its independent ciphertexts:
 
-* conv / dense  -> ``heb_dot_tensor`` (all output cells x all taps, lazy 128-bit
-                   accumulation) + one batched ``heb_relin_rescale``
-                   (+ broadcast bias adds);
-* square        -> ``heb_tensor`` + ``heb_relin_rescale``;
-* poly act      -> square path + two batched ct x pt rescales + adds
-                   (reference ``approx_relu_cell``);
-* sum pool      -> ``heb_sum_gather`` over the 2x2 windows;
+* conv          -> ``heb_conv``: fused tensor over every window (weights staged in
+                   shared memory), one batched relinearise + rescale, bias;
+* dense         -> ``heb_fc``: index-driven tensor (lazy 128-bit accumulation),
+                   relinearise + rescale, bias;
+* square        -> ``heb_square`` (tensor + relinearise + rescale);
+* poly act      -> ``heb_poly_act`` (reference ``approx_relu_cell``: square, two
+                   ct x pt rescales, adds);
+* sum pool      -> ``heb_sumpool`` over the 2x2 windows;
 * flatten       -> index remapping only (no data movement).
 
 Ciphertext bits, levels, exact scales, noise estimates and op counters are
@@ -138,22 +139,38 @@ class LayerEvaluator:
         self.be.counters.bump(ctct_mult=n_out * taps, ctct_add=n_out * (taps - 1))
         return raw, lvl, a.scale * b.scale, noise
 
-    def conv_dot(self, a: CipherBatch, w: CipherBatch, c_in: int, m: int, n: int, layer: Conv, n_out: int, taps: int):
-        """Fused convolution tensor (heb_conv_tensor): weights staged in shared memory."""
-        lvl = min(a.level, w.level)
+    def conv_layer(self, x: CipherBatch, w: CipherBatch, bias, c_in: int, m: int, n: int, layer: Conv, n_out: int,
+                   taps: int) -> CipherBatch:
+        """The whole conv layer (tensor over every window, relinearise + rescale, bias) as
+        one heb_conv call; weights staged in shared memory by the fused tensor kernel."""
+        lvl = min(x.level, w.level)
         if lvl < 1:
             raise DepthExhausted("ciphertext-ciphertext multiply at level 0")
-        k = lvl + 1
-        raw = self._empty(n_out, 3, k)
-        p, q = layer.kernel
-        self.ctx.call("heb_conv_tensor", a.desc(), w.desc(), ct_desc(raw), c_in, m, n, layer.filters, p, q,
-                      layer.stride, k, self.ctx.stream)
-        term = noise_sum(a.noise_bits, w.noise_bits)
+        term = noise_sum(x.noise_bits, w.noise_bits)
         if term > float("-inf"):
             term += 1.0
         noise = term + math.log2(taps) if term > float("-inf") else term
+        out_level, scale, noise = self._finalize_meta(lvl, x.scale * w.scale, noise)
+        in_c = bias is not None and bias.level >= out_level
+        if bias is not None and bias.scale != scale:
+            raise ScaleMismatch("batched add requires equal scales")
+        out = self._empty(n_out, 2, lvl)
+        evk = self.be._require_eval_key().evaluation
+        p, q = layer.kernel
+        bdesc = bias.desc() if in_c else _lib.HebCt(None, 0, 0)
+        self.ctx.call("heb_conv", x.desc(), w.desc(), bdesc, ct_desc(out), c_in, m, n, layer.filters, p, q,
+                      layer.stride, lvl, evk.prep.data_ptr(), self.ctx.stream)
         self.be.counters.bump(ctct_mult=n_out * taps, ctct_add=n_out * (taps - 1))
-        return raw, lvl, a.scale * w.scale, noise
+        y = CipherBatch(out, out_level, scale, noise)
+        if bias is None:
+            return y
+        per = n_out // layer.filters
+        if not in_c:  # bias below the output level: the sum drops to the bias level
+            for f in range(layer.filters):
+                self.add(y, bias_item(bias, f), b_broadcast=True, count=per, a_off=f * per, out=y, out_off=f * per)
+        else:
+            self.be.counters.bump(ctct_add=n_out)
+        return CipherBatch(y.buf, min(y.level, bias.level), y.scale, noise_sum(y.noise_bits, bias.noise_bits))
 
     def finalize(self, raw: torch.Tensor, level: int, scale: Fraction, noise: float) -> CipherBatch:
         evk = self.be._require_eval_key().evaluation
@@ -161,8 +178,7 @@ class LayerEvaluator:
         out = self._empty(n_out, 2, level)
         self.ctx.call("heb_relin_rescale", ct_desc(raw), evk.prep.data_ptr(), ct_desc(out), n_out, level,
                       self.ctx.stream)
-        new_scale = self.be._rescale_scale(scale, level)
-        return CipherBatch(out, level - 1, new_scale, max(noise, self.be._round_noise_bits(new_scale)))
+        return CipherBatch(out, *self._finalize_meta(level, scale, noise))
 
     def add(self, a: CipherBatch, b: CipherBatch, b_broadcast: bool = False, count: int | None = None,
             a_off: int = 0, out: CipherBatch | None = None, out_off: int = 0) -> CipherBatch:
@@ -183,27 +199,43 @@ class LayerEvaluator:
         self.be.counters.bump(ctct_add=n)
         return CipherBatch(dst, lvl, a.scale, noise_sum(a.noise_bits, b.noise_bits))
 
+    # -- ledger (level / exact scale / noise) of each op, shared by the primitive and the
+    #    layer entry points so both paths produce identical CipherBatch metadata ----------
+    def _finalize_meta(self, level: int, scale: Fraction, noise: float) -> tuple:
+        new_scale = self.be._rescale_scale(scale, level)
+        return level - 1, new_scale, max(noise, self.be._round_noise_bits(new_scale))
+
+    @staticmethod
+    def _square_noise(y: CipherBatch) -> float:
+        if y.noise_bits == float("-inf"):
+            return y.noise_bits
+        return noise_sum(y.noise_bits, y.noise_bits) + 1.0
+
+    def _mul_plain_meta(self, y_level: int, y_scale: Fraction, y_noise: float, pt, values_mag: float) -> tuple:
+        if y_level < 1:
+            raise DepthExhausted("ciphertext-plaintext multiply at level 0")
+        scale = self.be._rescale_scale(y_scale * pt.scale, y_level)
+        noise = y_noise + max(0.0, math.log2(max(values_mag, 1e-300))) + 1.0
+        return y_level - 1, scale, max(noise, self.be._round_noise_bits(scale))
+
     def square(self, y: CipherBatch) -> CipherBatch:
+        """x^2 activation: heb_square (tensor + relinearise + rescale) in one call."""
         if y.level < 1:
             raise DepthExhausted("ciphertext-ciphertext multiply at level 0")
-        k = y.k
-        raw = self._empty(y.count, 3, k)
-        self.ctx.call("heb_tensor", y.desc(), y.desc(), ct_desc(raw), y.count, k, 0, self.ctx.stream)
+        lvl, scale, noise = self._finalize_meta(y.level, y.scale * y.scale, self._square_noise(y))
+        out = self._empty(y.count, 2, y.level)
+        evk = self.be._require_eval_key().evaluation
+        self.ctx.call("heb_square", y.desc(), ct_desc(out), y.count, y.level, evk.prep.data_ptr(), self.ctx.stream)
         self.be.counters.bump(ctct_mult=y.count)
-        term = y.noise_bits + 1.0 if y.noise_bits > float("-inf") else y.noise_bits
-        term = noise_sum(y.noise_bits, y.noise_bits) + 1.0 if y.noise_bits > float("-inf") else term
-        return self.finalize(raw, y.level, y.scale * y.scale, term)
+        return CipherBatch(out, lvl, scale, noise)
 
     def mul_plain(self, y: CipherBatch, pt, values_mag: float) -> CipherBatch:
-        if y.level < 1:
-            raise DepthExhausted("ciphertext-plaintext multiply at level 0")
+        meta = self._mul_plain_meta(y.level, y.scale, y.noise_bits, pt, values_mag)
         out = self._empty(y.count, 2, y.level)
         self.ctx.call("heb_rescale", y.desc(), pt.payload.rows.data_ptr(), 0, ct_desc(out), y.count, 2, y.level,
                       self.ctx.stream)
         self.be.counters.bump(ctpt_mult=y.count)
-        scale = self.be._rescale_scale(y.scale * pt.scale, y.level)
-        noise = y.noise_bits + max(0.0, math.log2(max(values_mag, 1e-300))) + 1.0
-        return CipherBatch(out, y.level - 1, scale, max(noise, self.be._round_noise_bits(scale)))
+        return CipherBatch(out, *meta)
 
     def add_plain(self, y: CipherBatch, pt) -> CipherBatch:
         if pt.scale != y.scale:
@@ -231,8 +263,8 @@ class LayerEvaluator:
             ib = ((f * c_in + c) * p + dp) * q + dq
             return np.stack([ia.reshape(n_out, taps), ib.reshape(n_out, taps)])
 
-        if self.fused_conv and taps <= 64:
-            raw, lvl, scale, noise = self.conv_dot(x, w, c_in, m, n, layer, n_out, taps)
+        if self.fused_conv:
+            return self.conv_layer(x, w, bias, c_in, m, n, layer, n_out, taps), (F, om, on)
         else:
             idx = self._idx(("conv", dims, layer.kernel, s, F), build)
             raw, lvl, scale, noise = self.dot(x, w, idx[0], idx[1], taps, n_out)
@@ -251,11 +283,24 @@ class LayerEvaluator:
             pts = self._pt_cache[key] = act_plaintexts(self.be, act, y.level, y.scale)
         pt_quad, pt_lin, pt_const = pts
         c0, c1, c2 = act.folded()
-        t = self.square(y)
-        quad = self.mul_plain(t, pt_quad, abs(c2))
-        lin = self.mul_plain(y, pt_lin, abs(c1))
-        r = self.add(quad, lin)
-        return self.add_plain(r, pt_const)
+        # ledger of approx_relu_cell: t = y^2, quad = t (*) pt_quad, lin = y (*) pt_lin,
+        # r = quad + lin (at quad's level), r + pt_const
+        t_meta = self._finalize_meta(y.level, y.scale * y.scale, self._square_noise(y))
+        q_lvl, q_scale, q_noise = self._mul_plain_meta(*t_meta, pt_quad, abs(c2))
+        l_lvl, l_scale, l_noise = self._mul_plain_meta(y.level, y.scale, y.noise_bits, pt_lin, abs(c1))
+        if q_scale != l_scale:
+            raise ScaleMismatch("batched add requires equal scales")
+        if pt_const.scale != q_scale:
+            raise ScaleMismatch("plaintext addend must be encoded at the ciphertext scale")
+        lvl = min(q_lvl, l_lvl)
+        noise = noise_sum(noise_sum(q_noise, l_noise), self.be._encode_noise_bits())
+        out = self._empty(y.count, 2, lvl + 1)
+        evk = self.be._require_eval_key().evaluation
+        self.ctx.call("heb_poly_act", y.desc(), pt_quad.payload.rows.data_ptr(), pt_lin.payload.rows.data_ptr(),
+                      pt_const.payload.rows.data_ptr(), ct_desc(out), y.count, y.level, evk.prep.data_ptr(),
+                      self.ctx.stream)
+        self.be.counters.bump(ctct_mult=y.count, ctpt_mult=2 * y.count, ctct_add=y.count, ctpt_add=y.count)
+        return CipherBatch(out, lvl, q_scale, noise)
 
     def sum_pool(self, y: CipherBatch, dims: tuple[int, int, int]) -> tuple:
         c_in, m, n = dims
@@ -267,9 +312,9 @@ class LayerEvaluator:
             terms = [c * (m * n) + (2 * i + di) * n + (2 * j + dj) for di, dj in WINDOW_ORDER]
             return np.stack([t.ravel() for t in terms], axis=1)
 
-        idx = self._idx(("pool", dims), build)
+        del build  # the window indices are arithmetic inside heb_sumpool (WINDOW_ORDER sums are exact mod p)
         out = self._empty(n_out, 2, y.k)
-        self.ctx.call("heb_sum_gather", y.desc(), idx.data_ptr(), 4, ct_desc(out), n_out, 2, y.k, self.ctx.stream)
+        self.ctx.call("heb_sumpool", y.desc(), ct_desc(out), c_in, m, n, y.level, self.ctx.stream)
         self.be.counters.bump(ctct_add=3 * n_out)
         noise = y.noise_bits
         for _ in range(3):
@@ -285,11 +330,32 @@ class LayerEvaluator:
             return np.stack([ia, ib])
 
         idx = self._idx(("dense", din, dout, flat_map.tobytes()), build)
-        raw, lvl, scale, noise = self.dot(x, w, idx[0], idx[1], din, dout)
-        y = self.finalize(raw, lvl, scale, noise)
-        if bias is not None:
-            y = self.add(y, bias)
-        return y
+        lvl = min(x.level, w.level)
+        if lvl < 1:
+            raise DepthExhausted("ciphertext-ciphertext multiply at level 0")
+        term = noise_sum(x.noise_bits, w.noise_bits)
+        if term > float("-inf"):
+            term += 1.0
+        noise = term + math.log2(din) if term > float("-inf") else term
+        out_level, scale, noise = self._finalize_meta(lvl, x.scale * w.scale, noise)
+        in_c = bias is not None and bias.level >= out_level
+        if bias is not None and bias.scale != scale:
+            raise ScaleMismatch("batched add requires equal scales")
+        out = self._empty(dout, 2, lvl)
+        evk = self.be._require_eval_key().evaluation
+        ua, ub = self._unique.get(idx[0].data_ptr(), (dout * din, dout * din))
+        _lib.prof_next_bytes(8.0 * self.be.n * (lvl + 1) * (2 * ua + 2 * ub + 3 * dout))
+        self.ctx.call("heb_fc", x.desc(), w.desc(), idx[0].data_ptr(), idx[1].data_ptr(), din,
+                      bias.desc() if in_c else _lib.HebCt(None, 0, 0), ct_desc(out), dout, lvl, evk.prep.data_ptr(),
+                      self.ctx.stream)
+        self.be.counters.bump(ctct_mult=dout * din, ctct_add=dout * (din - 1))
+        y = CipherBatch(out, out_level, scale, noise)
+        if bias is None:
+            return y
+        if not in_c:
+            return self.add(y, bias)
+        self.be.counters.bump(ctct_add=dout)
+        return CipherBatch(out, min(y.level, bias.level), scale, noise_sum(noise, bias.noise_bits))
 
     def run(self, enc: EncryptedNetworkBatch, x: CipherBatch) -> CipherBatch:
         net = enc.net

@@ -324,3 +324,31 @@ def test_graph_pipelines_match_direct_run(golden, dev_s128, pipelines):
     torch.cuda.synchronize()
     assert all(torch.equal(h, want_rows[:, :, : want.k].cpu()) for h in host_out)
     assert be.counters.snapshot().__dict__ == {f: 4 * v for f, v in per_run.items()}
+
+
+def test_conv_beyond_fused_stage_matches_percell(dev_s128):
+    """heb_conv with more taps than the fused kernel's shared-memory stage (81 > 64):
+    window indices built on the device, index-driven tensor; bit-identical to the
+    reference op sequence (percell) and to the host-indexed gather-dot path."""
+    from paper_2102_00319_b200 import layers, percell
+    from paper_2102_00319_b200.model import Conv, Dense, Flatten, Network, Square, SumPool
+
+    be, keys = dev_s128
+    rng = np.random.default_rng(5)
+    net = Network((12, 12), (
+        Conv(weights=rng.normal(0, 0.1, (2, 1, 9, 9)), stride=1, bias=rng.normal(0, 0.1, 2)),
+        Square(), SumPool(), Flatten(),
+        Dense(weights=rng.normal(0, 0.3, (8, 3))),
+    ))
+    imgs = rng.uniform(0, 1, (be.slots, 12, 12))
+    enc = layers.encrypt_network(be, net, keys)
+    x = layers.encrypt_images(be, imgs, keys)
+    fused = layers.LayerEvaluator(be, fused_conv=True).run(enc, x)
+    generic = layers.LayerEvaluator(be, fused_conv=False).run(enc, x)
+    penc = percell.encrypt_network(be, net, keys)
+    logits = percell.run_network(be, penc, percell.encrypt_images(be, imgs, keys))
+    for i in range(fused.count):
+        a = np.concatenate(be.cipher_rows_host(be.batch_to_cipher(fused, i)))
+        b = np.concatenate(be.cipher_rows_host(be.batch_to_cipher(generic, i)))
+        c = np.concatenate(host(be, logits[i]))
+        assert np.array_equal(a, b) and np.array_equal(a, c)
