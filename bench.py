@@ -138,6 +138,7 @@ def run_gpu(args) -> None:
 
     from paper_2102_00319_b200 import _lib, layers
     from paper_2102_00319_b200.backend import B200Backend
+    from paper_2102_00319_b200.comm import LogitGather
     from paper_2102_00319_b200.configs import BATCH, CONFIGS, IMAGE_SEEDS, NETWORKS, cnn_images
     from paper_2102_00319_b200.model import plaintext_forward
 
@@ -161,11 +162,12 @@ def run_gpu(args) -> None:
         if world > 1:
             dist.barrier()
 
+    # logit ciphertexts of every rank gathered over NCCL by libheb200 (heb_gather_logits)
+    gatherer = LogitGather(world, rank, local) if world > 1 else None
+
     def gather(out):
-        if world > 1:
-            buf = torch.empty((world, *out.buf.shape), dtype=out.buf.dtype, device=out.buf.device)
-            dist.all_gather_into_tensor(buf, out.buf.contiguous())
-            return buf
+        if gatherer is not None:
+            return gatherer.gather(out.buf)
         return out.buf
 
     # correctness spot check against the float64 plaintext oracle (tolerance 1e-3, north star)
@@ -340,6 +342,8 @@ def run_gpu(args) -> None:
             "check": {"max_abs_err_vs_plaintext": err, "argmax_identical": argmax_ok, "images_checked": 256},
         }
         print(json.dumps(line), flush=True)
+    if gatherer is not None:
+        gatherer.close()
     if world > 1:
         dist.destroy_process_group()
 

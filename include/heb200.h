@@ -185,6 +185,20 @@ int heb_sumpool(heb_ctx *ctx, heb_ct y, heb_ct out, int channels, int m, int n, 
 int heb_fc(heb_ctx *ctx, heb_ct x, heb_ct w, const int32_t *x_idx, const int32_t *w_idx, int taps, heb_ct bias,
            heb_ct out, int64_t n_out, int level, const uint64_t *evk, void *stream);
 
+/* --- multi-GPU: logit gather ------------------------------------------
+ * Ranks evaluate independent image batches with replicated keys; the only exchange is
+ * an all-gather of the output logit ciphertexts over NCCL (NVLink / NVSwitch).  NCCL is
+ * bound at run time (libnccl.so.2, preferring the copy already loaded in the process).
+ * Replaces the reference's in-process fork-join combine (executor.py:161-279), which
+ * has no network transport. */
+typedef struct heb_comm heb_comm;
+/* 128-byte NCCL unique id, created on one rank and shared with the others by the host. */
+int heb_comm_unique_id(uint8_t *id_out);
+int heb_comm_init(heb_comm **out, const uint8_t *id, int nranks, int rank, int device);
+int heb_comm_destroy(heb_comm *comm);
+/* recv[r*words + i] = rank r's send[i] (ncclAllGather of u64 words on `stream`). */
+int heb_gather_logits(heb_comm *comm, const uint64_t *send, uint64_t *recv, int64_t words, void *stream);
+
 /* --- transport (host <-> device wire format) --------------------------------------- */
 /* Residue rows bit-packed at bitlen(p_r) bits per residue: a block of rows 0..rows-1
  * takes heb_packed_words(rows) words (row r: ceil(N*bitlen(p_r)/64) words, in order);

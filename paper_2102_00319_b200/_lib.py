@@ -68,6 +68,10 @@ SIGNATURES: dict[str, list] = {
     "heb_poly_act": [_P, _CT, _P, _P, _P, _CT, _L, _I, _P, _P],
     "heb_sumpool": [_P, _CT, _CT, _I, _I, _I, _I, _P],
     "heb_fc": [_P, _CT, _CT, _P, _P, _I, _CT, _CT, _L, _I, _P, _P],
+    "heb_comm_unique_id": [_P],
+    "heb_comm_init": [ctypes.POINTER(_P), _P, _I, _I, _I],
+    "heb_comm_destroy": [_P],
+    "heb_gather_logits": [_P, _P, _P, _L, _P],
     "heb_packed_words": [_P, _I],
     "heb_pack_rows": [_P, _P, _L, _I, _L, _P, _P],
     "heb_unpack_rows": [_P, _P, _L, _I, _P, _L, _P],

@@ -64,7 +64,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 if verbose:
                     print("compiled", os.path.relpath(src, REPO))
     if force or jobs or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-ldl"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr[-4000:]}")

@@ -16,5 +16,5 @@ for src in "$repo"/paper_2102_00319_b200/csrc/*.cu; do
   pids+=($!)
 done
 for p in "${pids[@]}"; do wait "$p" || { echo "variant $name: compile failed"; grep -m5 error "$obj"/*.log; exit 1; }; done
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o "$out/libheb200_$name.so" "$obj"/*.o
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o "$out/libheb200_$name.so" "$obj"/*.o -ldl
 echo "built $out/libheb200_$name.so"
