@@ -371,9 +371,9 @@ def cfg1_mulrelin(args, device: int) -> dict:
         be.ctx.call("heb_tensor", a.desc(), b.desc(), ct_desc(raw), 256, k, 0, be.ctx.stream)
         return ev.finalize(raw, a.level, a.scale * b.scale, 0.0)
 
-    for _ in range(3):
+    for _ in range(10):
         step()
-    reps = 20
+    reps = 200  # ~0.5 ms per call: enough calls for a stable rate
     torch.cuda.synchronize()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record()

@@ -130,6 +130,25 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_head(Ctx K, heb_ct src, int comp, i64 *D, 
 //   k_ks_modup_mac : pointwise, acc_t = sum_j v_j (*) key[j][t] with v_t = d2_t
 //                    (the centred digit is congruent to d2_t mod its own prime).
 // V layout: (count, k+1, k, N); slot (t, t) is unused.
+// ModUp input: digit D_j (centred mod q_j, int64) as a canonical residue mod p_t.  The
+// reference converts it to Montgomery form first (to_mont, kernels.py:297-340); here the
+// factor R lives in the prepared key instead (k_prep_key), and NTT_t is linear, so the
+// key products are the same residues.  When q_j / 2 < p_t the centred digit already lies
+// in (-p_t, p_t) and needs only a sign fix -- every digit except a wide base digit
+// entering a 40-bit target.
+struct DigitLoad {
+    const i64 *d;
+    u64 p, r1s;
+    bool small;
+    __device__ __forceinline__ DigitLoad(const i64 *d_, const PrimeInfo &P, u64 qj)
+        : d(d_), p(P.p), r1s(P.r1s), small((qj >> 1) < P.p) {}
+    __device__ __forceinline__ u64 operator()(int i) const {
+        const i64 v = __ldcg(d + i);
+        if (small) return (u64)v + (v < 0 ? p : 0);
+        return signed_mul_const(v, 1, r1s, p);
+    }
+};
+
 template <int LOGN>
 __global__ void ROW_BOUNDS(LOGN)
     k_ks_modup_ntt(Ctx K, const i64 *D, int k, u64 *V, int64_t count) {
@@ -165,7 +184,8 @@ __global__ void ROW_BOUNDS(LOGN)
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         const i64 *dj = D + (b * k + j) * n;
         u64 y[16];
-        fwd_any<LOGN>(K, gt, P, sm, [&](int i) { return signed_mul_const(__ldcg(dj + i), P.rmod, P.rmod_s, P.p); }, y);
+        DigitLoad ld(dj, P, K.pi[j].p);
+        fwd_any<LOGN>(K, gt, P, sm, ld, y);
         store16<LOGN>(V + ((b * (k + 1) + t) * k + j) * n + tpos<LOGN>(), y);
     }
 }
@@ -327,7 +347,7 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : NT
                 load16<LOGN>(at(src, b, comp, t, LOGN) + pos, y);  // d2_t: congruent digit, no transform
             } else {
                 const i64 *dj = D + (b * k + j) * n;
-                auto ld = [&](int i) { return signed_mul_const(__ldcg(dj + i), P.rmod, P.rmod_s, P.p); };
+                DigitLoad ld(dj, P, K.pi[j].p);
                 if constexpr (ENG == 0) {
                     fwd_any<LOGN>(K, gt, P, sm, ld, y);
                 } else {
@@ -454,7 +474,8 @@ __global__ void __launch_bounds__(256, MAC_MINB) k_ks_modup_mac(Ctx K, heb_ct sr
     }
 }
 
-// Prepared switching key: Montgomery residue x -> (w = x R^-1, floor(w 2^64 / p)).
+// Prepared switching key: Montgomery residue x of digit j, row r -> (w, floor(w 2^64 / p))
+// with w = x R^-1 on the diagonal j == r and w = x elsewhere (see DigitLoad).
 // floor(w 2^64/p) = w floor(2^64/p) + floor(w (2^64 mod p) / p), the last term by a
 // Shoup quotient with one correction -- exact, no 128-bit division.
 __global__ void k_prep_key(Ctx K, const u64 *kb, const u64 *ka, ulonglong2 *out, int digits, int logn) {
@@ -467,7 +488,11 @@ __global__ void k_prep_key(Ctx K, const u64 *kb, const u64 *ka, ulonglong2 *out,
         double *dstd = reinterpret_cast<double *>(out + (((size_t)j * K.num_rows + r) * 2) * n) + i;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-            const u64 w = mont_mul(c == 0 ? kb[src] : ka[src], 1, P.p, P.pinv);
+            // j == r: the digit is d2_r itself (Montgomery form) -> w = x R^-1;
+            // j != r: the ModUp digit enters without its Montgomery factor (DigitLoad),
+            // so the key keeps it: w = x
+            const u64 x = c == 0 ? kb[src] : ka[src];
+            const u64 w = j == r ? mont_mul(x, 1, P.p, P.pinv) : x;
             if (P.use_fp) {  // FP64 rows: w as a double, b part then a part
                 dstd[(size_t)c * n] = (double)w;
                 continue;
