@@ -26,19 +26,26 @@ static bool getenv_flag(const char *name) {
 namespace {
 constexpr int XC = 32;  // positions per CTA (one warp-width)
 constexpr int SW = 8;   // workers per position  -> 256 threads
-constexpr int FG = 5;   // filters per CTA group
+#ifndef CONV_FGF
+#define CONV_FGF 5
+#endif
+constexpr int FG = CONV_FGF;  // filters per CTA group
 }  // namespace
+#ifndef CONV_MINB
+#define CONV_MINB 2
+#endif
 
 // One CTA = (row r, XC positions from bx * XC, filter group): integer rows (and, without
 // the split-limb path, FP64 rows with one exact FP64 modular product per term).
+// Output cells [cell_lo, cell_hi) of row r (the integer rows split their cells over
+// several CTAs, see k_conv_tensor).
 template <bool FLUSH, bool ALLOW_FP>
 __device__ __forceinline__ void conv_body(u64 *wsm, const Ctx &K, const heb_ct &A, const heb_ct &B, const heb_ct &D,
                                           int C, int m, int n, int F, int P, int Q, int s, int om, int on, int logn,
-                                          int flush, int bx) {
+                                          int flush, int bx, int r, int cell_lo, int cell_hi) {
     // wsm: [tap][fl][comp][XC]
     const int xl = threadIdx.x % XC, w = threadIdx.x / XC;
     const int x = bx * XC + xl;
-    const int r = blockIdx.y;
     const int f0 = blockIdx.z * FG;
     const int nf = min(FG, F - f0);
     const int taps = C * P * Q;
@@ -69,7 +76,7 @@ __device__ __forceinline__ void conv_body(u64 *wsm, const Ctx &K, const heb_ct &
         // factor of the reference's mont_mul accumulation.
         const double pd = Pr.pd, pinvd = Pr.pinvd, rinv = (double)Pr.rinv;
         const double *wd = reinterpret_cast<const double *>(wsm);
-        for (int cell = w; cell < cells; cell += SW) {
+        for (int cell = cell_lo + w; cell < cell_hi; cell += SW) {
             const int i = cell / on, j = cell % on;
             double s0[FG], s1[FG], s2[FG];
 #pragma unroll
@@ -110,7 +117,7 @@ __device__ __forceinline__ void conv_body(u64 *wsm, const Ctx &K, const heb_ct &
         }
         return;
     }
-    for (int cell = w; cell < cells; cell += SW) {
+    for (int cell = cell_lo + w; cell < cell_hi; cell += SW) {
         const int i = cell / on, j = cell % on;
         acc4 s0[FG], s1[FG], s2[FG];
         u64 t0[FG], t1[FG], t2[FG];
@@ -178,9 +185,6 @@ __device__ __forceinline__ void conv_body(u64 *wsm, const Ctx &K, const heb_ct &
 namespace {
 constexpr int XF = 16;  // positions per CTA
 constexpr int SF = 16;  // workers per position -> 256 threads
-#ifndef CONV_FGF
-#define CONV_FGF 5
-#endif
 constexpr int FGF = CONV_FGF;  // filters per CTA group
 constexpr int FP_MAX_TAPS = 256;
 constexpr u64 M20 = (1ull << 20) - 1;
@@ -188,10 +192,9 @@ constexpr u64 M20 = (1ull << 20) - 1;
 
 __device__ __forceinline__ void conv_body_limbs(double *wl, const Ctx &K, const heb_ct &A, const heb_ct &B,
                                                 const heb_ct &D, int C, int m, int n, int F, int P, int Q, int s,
-                                                int om, int on, int logn) {
+                                                int om, int on, int logn, int bx, int r) {
     const int xl = threadIdx.x % XF, w = threadIdx.x / XF;
-    const int x = blockIdx.x * XF + xl;
-    const int r = blockIdx.y;
+    const int x = bx * XF + xl;
     const PrimeInfo Pr = K.pi[r];
     const int f0 = blockIdx.z * FGF;
     const int nf = min(FGF, F - f0);
@@ -282,20 +285,42 @@ __device__ __forceinline__ void conv_body_limbs(double *wl, const Ctx &K, const 
     }
 }
 
-// One launch for all rows: FP64 rows take the split-limb body (XF positions per CTA),
-// integer rows the 128-bit body (XC positions per CTA; the surplus x-blocks exit), so
-// the long integer-row CTAs run alongside the FP64-row CTAs.
+// Which CTA does what.  FP64 rows take the split-limb body (XF positions per CTA);
+// integer rows the 128-bit body (XC positions per CTA, cells split over `cs` CTAs so an
+// integer CTA lasts about as long as an FP64 one).  The integer CTAs are spread evenly
+// through the launch order, so they run on the IMAD pipe alongside FP64-row CTAs on the
+// DFMA pipe instead of occupying most SM slots in the first wave.
+struct ConvMap {
+    int nfp, nint;           // CTAs of each kind (per filter group)
+    int xf_blocks, xc_blocks, cs;
+    int8_t fp_rows[32], int_rows[32];
+};
+
 template <bool FLUSH, bool LIMBS>
-__global__ void __launch_bounds__(256, 2) k_conv_tensor(Ctx K, heb_ct A, heb_ct B, heb_ct D, int C, int m, int n,
+__global__ void __launch_bounds__(256, CONV_MINB) k_conv_tensor(Ctx K, heb_ct A, heb_ct B, heb_ct D, int C, int m, int n,
                                                          int F, int P, int Q, int s, int om, int on, int logn,
-                                                         int flush) {
+                                                         int flush, ConvMap map) {
     extern __shared__ u64 conv_smem[];
-    if (LIMBS && K.pi[blockIdx.y].use_fp) {
-        conv_body_limbs(reinterpret_cast<double *>(conv_smem), K, A, B, D, C, m, n, F, P, Q, s, om, on, logn);
+    const int cells = om * on;
+    if (!LIMBS) {
+        conv_body<FLUSH, true>(conv_smem, K, A, B, D, C, m, n, F, P, Q, s, om, on, logn, flush, blockIdx.x,
+                               blockIdx.y, 0, cells);
         return;
     }
-    if (LIMBS && (int)blockIdx.x >= ((1 << logn) / XC)) return;
-    conv_body<FLUSH, !LIMBS>(conv_smem, K, A, B, D, C, m, n, F, P, Q, s, om, on, logn, flush, blockIdx.x);
+    const int b = blockIdx.x, total = map.nfp + map.nint;
+    const int ib = (int)(((long)b * map.nint) / total);
+    const bool is_int = ((long)(b + 1) * map.nint) / total != ib;
+    if (is_int) {
+        const int per_row = map.xc_blocks * map.cs;
+        const int rem = ib % per_row, split = rem % map.cs;
+        conv_body<FLUSH, false>(conv_smem, K, A, B, D, C, m, n, F, P, Q, s, om, on, logn, flush, rem / map.cs,
+                                map.int_rows[ib / per_row], (int)((long)split * cells / map.cs),
+                                (int)((long)(split + 1) * cells / map.cs));
+    } else {
+        const int fb = b - ib;
+        conv_body_limbs(reinterpret_cast<double *>(conv_smem), K, A, B, D, C, m, n, F, P, Q, s, om, on, logn,
+                        fb % map.xf_blocks, map.fp_rows[fb / map.xf_blocks]);
+    }
 }
 
 extern "C" int heb_conv_tensor(heb_ctx *c, heb_ct a, heb_ct b, heb_ct d, int channels, int m, int n, int filters,
@@ -312,15 +337,32 @@ extern "C" int heb_conv_tensor(heb_ctx *c, heb_ct a, heb_ct b, heb_ct d, int cha
     const bool limbs = taps <= FP_MAX_TAPS && !getenv_flag("HEB_CONV_NO_LIMBS");
     const size_t smf = sizeof(double) * (size_t)taps * FGF * 4 * XF;
     const size_t smem = limbs ? std::max(sm, smf) : sm;
-    const dim3 grid(c->n / (limbs ? XF : XC), k, (filters + FG - 1) / FG);
     static_assert(FG == FGF, "both bodies use the same filter groups");
+    ConvMap map{};
+    map.xf_blocks = c->n / XF;
+    map.xc_blocks = c->n / XC;
+    static const int cs_env = [] {
+        const char *e = getenv("HEB_CONV_CS");
+        return e ? std::max(1, atoi(e)) : 4;
+    }();
+    map.cs = cs_env;
+    if (k > 32) return fail(HEB_EUNSUP, "heb_conv_tensor: more than 32 rows");
+    int nfr = 0, nir = 0;
+    for (int r = 0; r < k; ++r) {
+        if (c->row_fp[r]) map.fp_rows[nfr++] = (int8_t)r;
+        else map.int_rows[nir++] = (int8_t)r;
+    }
+    map.nfp = nfr * map.xf_blocks;
+    map.nint = nir * map.xc_blocks * map.cs;
+    const dim3 grid = limbs ? dim3(map.nfp + map.nint, 1, (filters + FG - 1) / FG)
+                            : dim3(c->n / XC, k, (filters + FG - 1) / FG);
     const double nout = (double)filters * om * on;
     PROF("k_conv_tensor", st, 8.0 * c->n * k * (2.0 * channels * m * n + 2.0 * filters * taps + 3.0 * nout));
 #define CONV_LAUNCH(FL, LI)                                                                                   \
     {                                                                                                         \
         CUDA_TRY(prep_kernel(k_conv_tensor<FL, LI>, smem));                                                   \
         k_conv_tensor<FL, LI><<<grid, 256, smem, st>>>(kctx(c), a, b, d, channels, m, n, filters, kp, kq, stride, \
-                                                       om, on, c->log_n, c->flush);                          \
+                                                       om, on, c->log_n, c->flush, map);                     \
     }
     if (limbs) {
         if (need_flush) CONV_LAUNCH(true, true) else CONV_LAUNCH(false, true)
