@@ -728,7 +728,8 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
         { PROF("k_ks_head", st, 16.0 * n * cnt * k); CUDA_TRY(launch_by_engine<LOGN>(c, ENGINE_KERNELS(k_ks_head), 0, k, gy, 1, sm, st, K, s, comp, (i64 *)sD.p, k, cnt)); }
         LAUNCH_CHECK();
         if (fused) {
-            PROF("k_ks_modup_fused", st, 8.0 * n * cnt * ((double)k + 4.0 * k * (k + 1) / cnt + 2.0 * (k + 1)));
+            // algorithmic: read D (k rows) and the congruent d2 rows (k), the key once, write acc (2(k+1) rows)
+            PROF("k_ks_modup_fused", st, 8.0 * n * cnt * (2.0 * k + 4.0 * k * (k + 1) / cnt + 2.0 * (k + 1)));
 #ifndef MODUP_ENGINES_SPLIT
 #define MODUP_ENGINES_SPLIT 1
 #endif
