@@ -69,6 +69,7 @@ extern "C" int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows
     if (log_n < 6 || log_n > 15) return fail(HEB_EUNSUP, "ring degree 2^%d not supported (2^6 .. 2^15)", log_n);
     const int n = 1 << log_n;
     auto *c = new heb_ctx();
+    if (const char *e = getenv("HEB_CHUNK")) c->chunk = std::max(1, atoi(e));  // key-switch chunk override
     c->device = device;
     c->log_n = log_n;
     c->n = n;
