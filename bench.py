@@ -176,6 +176,10 @@ def run_gpu(args) -> None:
     ref = plaintext_forward(net, images[:256])
     err = float(np.max(np.abs(dec[:256] - ref)))
     argmax_ok = bool(np.array_equal(np.argmax(dec[:256], 1), np.argmax(ref, 1)))
+    out_count, out_k = out.count, out.k
+    del out
+    be.ctx.release_scratch()  # the check ran on the default stream; the pipelines use their own
+    torch.cuda.empty_cache()
 
     clocks = Clocks(local)
     clocks.start()
@@ -217,14 +221,17 @@ def run_gpu(args) -> None:
         torch.cuda.synchronize()
         p0 = torch.cuda.Event(enable_timing=True)
         p1 = torch.cuda.Event(enable_timing=True)
-        p0.record(stream)
-        for _ in range(args.steps):
-            gather(ev.run(enc, x))
-        p1.record(stream)
+        pst = ev.pipeline_stream(0)  # pipeline 0's stream: its scratch arena already exists
+        with torch.cuda.stream(pst):
+            p0.record(pst)
+            for _ in range(args.steps):
+                gather(ev.run(enc, x))
+            p1.record(pst)
         torch.cuda.synchronize()
         prof = _lib.prof_summary()
         _lib.prof_enable(False)
         prof_ms = p0.elapsed_time(p1)
+        torch.cuda.empty_cache()
     launches = sum(v[0] for v in prof.values())
 
     # ---- end-to-end: host buffers through the public API -------------------------------
@@ -237,7 +244,7 @@ def run_gpu(args) -> None:
     for h in x_hosts:
         h.copy_(x_packed)
     del x_packed
-    logits_hosts = [torch.empty((out.count, 2, out.k, be.n), dtype=torch.int64, pin_memory=True)
+    logits_hosts = [torch.empty((out_count, 2, out_k, be.n), dtype=torch.int64, pin_memory=True)
                     for _ in range(args.steps)]
 
     def e2e_run(nsteps):
@@ -334,7 +341,7 @@ def run_gpu(args) -> None:
                 "unit": UNIT,
                 "h2d_bytes_per_step": int(x_hosts[0].numel() * 8),
                 "wire_format": "bit-packed residues (heb_pack_rows), unpacked on the device in the step",
-                "d2h_bytes_per_step": int(out.count * 2 * out.k * be.n * 8),
+                "d2h_bytes_per_step": int(out_count * 2 * out_k * be.n * 8),
             },
             "gpu_launches": int(launches),
             "clocks": clk,

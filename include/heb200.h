@@ -58,6 +58,9 @@ int heb_ctx_ring_degree(const heb_ctx *ctx);
 /* Key-switch / rescale batches are processed in chunks of this many items
  * (default 1024), bounding the stream-ordered scratch. */
 int heb_ctx_set_chunk(heb_ctx *ctx, int items);
+/* Free the scratch arena of `stream` (after synchronising it); the next call on that
+ * stream grows a new one.  For one-off evaluations on streams that will not be reused. */
+int heb_ctx_release_scratch(heb_ctx *ctx, void *stream);
 
 /* --- memory ----------------------------------------------------------------- */
 int heb_alloc(size_t bytes, void **out, void *stream);

@@ -36,6 +36,7 @@ SIGNATURES: dict[str, list] = {
     "heb_ctx_destroy": [_P],
     "heb_ctx_ring_degree": [_P],
     "heb_ctx_set_chunk": [_P, _I],
+    "heb_ctx_release_scratch": [_P, _P],
     "heb_alloc": [ctypes.c_size_t, ctypes.POINTER(_P), _P],
     "heb_free": [_P, _P],
     "heb_h2d": [_P, _P, ctypes.c_size_t, _P],

@@ -94,6 +94,10 @@ class DeviceContext:
     def set_chunk(self, items: int) -> None:
         _lib.call("heb_ctx_set_chunk", self.handle, items)
 
+    def release_scratch(self, stream=None) -> None:
+        """Free the scratch arena of ``stream`` (default: this context's stream)."""
+        _lib.call("heb_ctx_release_scratch", self.handle, self.stream if stream is None else stream)
+
     def __del__(self):
         h = getattr(self, "handle", None)
         if h:

@@ -126,8 +126,10 @@ struct Scratch {
             ++a->blk;
             a->off = 0;
         }
-        size_t cap = a->blocks.empty() ? (size_t)64 << 20 : a->blocks.back().cap * 2;
-        if (cap < bytes) cap = bytes;
+        // a new block holds this request (at least 64 MB, 2 MB granules): no geometric
+        // growth, so a multi-GB layer intermediate does not double the arena's footprint
+        size_t cap = std::max(bytes, (size_t)64 << 20);
+        cap = (cap + ((size_t)2 << 20) - 1) & ~(((size_t)2 << 20) - 1);
         void *q = nullptr;
         cudaError_t e = cudaMalloc(&q, cap);
         if (e != cudaSuccess) return e;

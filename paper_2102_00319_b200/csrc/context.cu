@@ -221,6 +221,23 @@ extern "C" int heb_ctx_destroy(heb_ctx *c) {
     return HEB_OK;
 }
 
+extern "C" int heb_ctx_release_scratch(heb_ctx *c, void *stream) {
+    if (!c) return fail(HEB_EINVAL, "heb_ctx_release_scratch: null context");
+    StreamArena *a;
+    {
+        std::lock_guard<std::mutex> g(c->arena_mu);
+        auto it = c->arenas.find((cudaStream_t)stream);
+        if (it == c->arenas.end()) return HEB_OK;
+        a = it->second.get();
+    }
+    std::lock_guard<std::recursive_mutex> g(a->mu);
+    if (a->blk != 0 || a->off != 0) return fail(HEB_EINVAL, "heb_ctx_release_scratch: scratch in use");
+    CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));  // queued work may still read it
+    for (auto &b : a->blocks) cudaFree(b.base);
+    a->blocks.clear();
+    return HEB_OK;
+}
+
 extern "C" int heb_ctx_ring_degree(const heb_ctx *c) { return c ? c->n : 0; }
 extern "C" int heb_ctx_set_chunk(heb_ctx *c, int items) {
     if (!c || items < 1) return fail(HEB_EINVAL, "bad chunk");

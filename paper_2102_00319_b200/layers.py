@@ -388,6 +388,10 @@ class LayerEvaluator:
             pool.append(torch.cuda.Stream(self.be.dev))
         return pool[:count]
 
+    def pipeline_stream(self, pipeline: int) -> torch.cuda.Stream:
+        """The persistent compute stream of ``pipeline`` (its scratch arena is reused)."""
+        return self._pipeline_streams("compute", pipeline + 1)[pipeline]
+
     def captured(self, enc: EncryptedNetworkBatch, x: CipherBatch, pipeline: int):
         """(graph, output, counter delta) -- one inference of ``x`` captured as a CUDA graph.
 
