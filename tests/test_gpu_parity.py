@@ -352,3 +352,38 @@ def test_conv_beyond_fused_stage_matches_percell(dev_s128):
         b = np.concatenate(be.cipher_rows_host(be.batch_to_cipher(generic, i)))
         c = np.concatenate(host(be, logits[i]))
         assert np.array_equal(a, b) and np.array_equal(a, c)
+
+
+def test_layer_entry_points_edge_cases(dev_s128):
+    """Empty batches are no-ops; out-of-range levels and shapes fail loudly (ValueError
+    from HEB_EINVAL) instead of touching memory -- reference errors.py taxonomy."""
+    from paper_2102_00319_b200 import _lib
+    from paper_2102_00319_b200.backend import ct_desc
+
+    be, _ = dev_s128
+    ctx = be.ctx
+    evk = be._require_eval_key().evaluation.prep.data_ptr()
+    top = be.chain.num_rows - 2  # highest ciphertext level
+    buf = ctx.empty(2, 3, top + 1, be.n)
+    d = ct_desc(buf)
+    none = _lib.HebCt(None, 0, 0)
+    ctx.call("heb_square", d, d, 0, top, evk, ctx.stream)                      # count 0: no-op
+    ctx.call("heb_fc", d, d, buf.data_ptr(), buf.data_ptr(), 1, none, d, 0, top, evk, ctx.stream)
+    ctx.call("heb_poly_act", d, buf.data_ptr(), buf.data_ptr(), buf.data_ptr(), d, 0, top, evk, ctx.stream)
+    with pytest.raises(ValueError):
+        ctx.call("heb_square", d, d, 1, top + 1, evk, ctx.stream)              # no row to drop into
+    with pytest.raises(ValueError):
+        ctx.call("heb_square", d, d, 1, 0, evk, ctx.stream)                    # depth exhausted
+    with pytest.raises(ValueError):
+        ctx.call("heb_poly_act", d, buf.data_ptr(), buf.data_ptr(), buf.data_ptr(), d, 1, 1, evk, ctx.stream)
+    with pytest.raises(ValueError):
+        ctx.call("heb_conv", d, d, none, d, 1, 4, 4, 1, 5, 5, 1, top, evk, ctx.stream)  # kernel larger than map
+    with pytest.raises(ValueError):
+        ctx.call("heb_sumpool", d, d, 1, 1, 4, 0, ctx.stream)                  # map narrower than a window
+    torch_sync()
+
+
+def torch_sync():
+    import torch
+
+    torch.cuda.synchronize()
