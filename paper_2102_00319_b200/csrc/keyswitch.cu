@@ -216,7 +216,8 @@ __device__ __forceinline__ void tmem_ld8(uint32_t a, uint32_t (&v)[8]) {
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // accumulate y (*) key over this thread's 16 line-pair positions, 4 positions per TMEM access
-template <int LOGN, bool FP>
+// (RAW: FP64 rows hand y over as raw double bit patterns, FpArithRaw)
+template <int LOGN, bool FP, bool RAW = false>
 __device__ __forceinline__ void modup_acc(uint32_t ta, const u64 (&y)[16], const ulonglong2 *keyrow, int pos,
                                           bool first, const PrimeInfo &P) {
     const int n = 1 << LOGN;
@@ -234,8 +235,10 @@ __device__ __forceinline__ void modup_acc(uint32_t ta, const u64 (&y)[16], const
                 if constexpr (FP) {
                     const double *kd = reinterpret_cast<const double *>(keyrow) + (size_t)c * n;
                     const double2 kv = __ldg(reinterpret_cast<const double2 *>(kd + off));
-                    double a0 = ntt::fmul(ntt::u2d(y[2 * i]), kv.x, P.pd, P.pinvd);
-                    double a1 = ntt::fmul(ntt::u2d(y[2 * i + 1]), kv.y, P.pd, P.pinvd);
+                    const double y0 = RAW ? __longlong_as_double((long long)y[2 * i]) : ntt::u2d(y[2 * i]);
+                    const double y1 = RAW ? __longlong_as_double((long long)y[2 * i + 1]) : ntt::u2d(y[2 * i + 1]);
+                    double a0 = ntt::fmul(y0, kv.x, P.pd, P.pinvd);
+                    double a1 = ntt::fmul(y1, kv.y, P.pd, P.pinvd);
                     if (!first) {
                         a0 += __hiloint2double(w[4 * h + 1], w[4 * h]);
                         a1 += __hiloint2double(w[4 * h + 3], w[4 * h + 2]);
@@ -345,6 +348,10 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : NT
             u64 y[16];
             if (j == t) {
                 load16<LOGN>(at(src, b, comp, t, LOGN) + pos, y);  // d2_t: congruent digit, no transform
+                if constexpr (ENG == 1) {  // canonical residues -> the raw doubles FpArithRaw hands out
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) y[i] = (u64)__double_as_longlong(ntt::u2d(y[i]));
+                }
             } else {
                 const i64 *dj = D + (b * k + j) * n;
                 DigitLoad ld(dj, P, K.pi[j].p);
@@ -353,7 +360,7 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : NT
                 } else {
                     constexpr int LL = Row<LOGN>::LL;
                     if constexpr (ENG == 1) {
-                        const ntt::FpArith ar(P.pd, P.pinvd);
+                        const ntt::FpArithRaw ar(P.pd, P.pinvd);
                         double *s2 = reinterpret_cast<double *>(sm);
                         const double *tw = K.twf + ((size_t)gt << LOGN);
                         if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, 16>(ar, s2, tw, ld, y, rhalf<LOGN>());
@@ -367,7 +374,9 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : NT
                 }
             }
             const ulonglong2 *keyrow = key + (((size_t)j * R + gt) * 2) * n;
-            if (ENG == 1 || (ENG == 0 && HEB_FPSEL(P.use_fp)))
+            if (ENG == 1)
+                modup_acc<LOGN, true, true>(ta, y, keyrow, pos, first, P);
+            else if (ENG == 0 && HEB_FPSEL(P.use_fp))
                 modup_acc<LOGN, true>(ta, y, keyrow, pos, first, P);
             else
                 modup_acc<LOGN, false>(ta, y, keyrow, pos, first, P);

@@ -156,6 +156,14 @@ struct FpArith {
     }
 };
 
+// FP64 engine whose forward hands out raw (unreduced, signed, |v| < 2^47) doubles as bit
+// patterns instead of canonical residues: for consumers that multiply the transform by
+// fmul right away (fmul accepts such operands), e.g. the fused ModUp key products.
+struct FpArithRaw : FpArith {
+    HD FpArithRaw(double p_, double pinv_) : FpArith(p_, pinv_) {}
+    HD u64 out_fwd(V x) const { return (u64)__double_as_longlong(x); }
+};
+
 // ---------------------------------------------------------------- forward ----
 // One forward group: radix 2^RB covering stages S0 .. S0+RB-1.
 // SRC: 0 = functor load, 1 = shared memory.  DST: 0 = shared memory, 1 = registers.
