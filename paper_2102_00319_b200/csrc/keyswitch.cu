@@ -311,8 +311,11 @@ __host__ __device__ constexpr uint32_t modup_tmem_cols() {
 #ifndef MODUP_INT_MINB
 #define MODUP_INT_MINB(LOGN) NTT_MINB(LOGN)
 #endif
+#ifndef MODUP_FP_MINB
+#define MODUP_FP_MINB(LOGN) NTT_MINB(LOGN)
+#endif
 template <int LOGN, int ENG>
-__global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : NTT_MINB(LOGN)) k_ks_modup_fused(Ctx K, heb_ct src, int comp, const i64 *D, const ulonglong2 *key,
+__global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MODUP_FP_MINB(LOGN)) k_ks_modup_fused(Ctx K, heb_ct src, int comp, const i64 *D, const ulonglong2 *key,
                                                   int k, u64 *acc, int64_t count) {
     extern __shared__ u64 sm[];
     __shared__ uint32_t tbase;
