@@ -32,13 +32,27 @@ class LogitGather:
         handle = ctypes.c_void_p()
         _lib.call("heb_comm_init", ctypes.byref(handle), uid, world, rank, device)
         self.handle, self.world, self.rank = handle, world, rank
+        self._comm_stream = None
 
     def gather(self, logits: torch.Tensor, stream=None) -> torch.Tensor:
-        """(world, *logits.shape) on the device: every rank's logit ciphertexts."""
+        """(world, *logits.shape) on the device: every rank's logit ciphertexts.
+
+        Ordered after ``stream``'s work (default: the current stream), and the caller's
+        stream is ordered after the gather.  Collectives of one communicator must run in
+        the same order on every rank, so all of them go through one communication stream
+        even when several pipelines (streams) produce logits."""
         src = logits.contiguous()
-        out = torch.empty((self.world, *src.shape), dtype=src.dtype, device=src.device)
         st = stream if stream is not None else torch.cuda.current_stream(src.device)
-        _lib.call("heb_gather_logits", self.handle, src.data_ptr(), out.data_ptr(), src.numel(), st.cuda_stream)
+        if self._comm_stream is None:
+            self._comm_stream = torch.cuda.Stream(src.device)
+        cs = self._comm_stream
+        cs.wait_stream(st)
+        with torch.cuda.stream(cs):
+            out = torch.empty((self.world, *src.shape), dtype=src.dtype, device=src.device)
+            _lib.call("heb_gather_logits", self.handle, src.data_ptr(), out.data_ptr(), src.numel(), cs.cuda_stream)
+        src.record_stream(cs)
+        out.record_stream(st)
+        st.wait_stream(cs)
         return out
 
     def close(self) -> None:

@@ -43,3 +43,24 @@ def test_gathered_logits_decrypt_like_local(tmp_path):
     dec = be.decrypt_batch(CipherBatch(got, ct.level, ct.scale, ct.noise_bits), keys)
     assert np.array_equal(dec, be.decrypt_batch(ct, keys))
     del layers
+
+
+def test_gathers_from_several_pipeline_streams_keep_order():
+    """Logits produced on different pipeline streams are gathered through one
+    communication stream (NCCL collectives must run in issue order on every rank)."""
+    from paper_2102_00319_b200.comm import LogitGather
+
+    g = LogitGather(1, 0, 0)
+    try:
+        streams = [torch.cuda.Stream() for _ in range(3)]
+        xs = [torch.full((4, 2, 3, 4096), i, dtype=torch.int64, device="cuda") for i in range(6)]
+        outs = []
+        for i, x in enumerate(xs):
+            s = streams[i % 3]
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                outs.append(g.gather(x))
+        torch.cuda.synchronize()
+        assert all(torch.equal(o[0], x) for o, x in zip(outs, xs))
+    finally:
+        g.close()
