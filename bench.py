@@ -434,8 +434,14 @@ def ncu_pipes(kernel: str):
         rec = json.load(fh).get(kernel)
     if not rec:
         return None
-    keys = ("fp64_pipe_pct", "alu_pipe_pct", "fma_pipe_pct", "issue_active_pct", "source")
-    return {k: rec[k] for k in keys if k in rec}
+    keys = ("fp64_pipe_pct", "alu_pipe_pct", "fma_pipe_pct", "issue_active_pct", "traffic_over_algorithmic", "source")
+    out = {k: rec[k] for k in keys if k in rec}
+    # per device launch (one per NTT engine for the fused ModUp): the pipe that bounds each
+    per = [{k: l[k] for k in ("name", "fp64_pipe_pct", "fma_pipe_pct", "alu_pipe_pct", "issue_active_pct") if k in l}
+           for l in rec.get("launches", [])]
+    if per:
+        out["per_launch"] = per
+    return out
 
 
 # ---------------------------------------------------------------------------
