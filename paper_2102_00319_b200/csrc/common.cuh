@@ -76,6 +76,10 @@ struct StreamArena {
     };
     std::recursive_mutex mu;
     std::vector<Block> blocks;
+    // side stream of this stream (created on first use, outside any capture) and the
+    // fork / join events that order it: independent launches of one call overlap on it
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
     size_t blk = 0, off = 0;  // bump position
 };
 

@@ -214,8 +214,14 @@ extern "C" int heb_ctx_destroy(heb_ctx *c) {
     cudaFree(c->d_last);
     if (!c->arenas.empty()) {
         cudaDeviceSynchronize();  // scratch may still be in use by queued work
-        for (auto &kv : c->arenas)
+        for (auto &kv : c->arenas) {
             for (auto &b : kv.second->blocks) cudaFree(b.base);
+            if (kv.second->side) {
+                cudaStreamDestroy(kv.second->side);
+                cudaEventDestroy(kv.second->fork);
+                cudaEventDestroy(kv.second->join);
+            }
+        }
     }
     delete c;
     return HEB_OK;
