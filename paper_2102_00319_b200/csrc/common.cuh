@@ -304,12 +304,36 @@ static cudaError_t launch_rows(Kern kernel, dim3 grid, int block, size_t smem, c
 // range (the usual chain layout: wide base prime first, 40-bit level primes after) the
 // rows are split over the integer-only and FP64-only instantiations, each register-
 // allocated on its own; otherwise the run-time dispatching instantiation covers all.
+// Fork `st`'s side stream off st (the side stream and its events are created on first
+// use, outside any graph capture) / join it back.  Work on the side stream between the
+// two overlaps the work on st.
+static inline cudaError_t side_fork(heb_ctx *c, cudaStream_t st, cudaStream_t *side) {
+    StreamArena *ar = c->arena(st);
+    std::lock_guard<std::recursive_mutex> g(ar->mu);
+    if (!ar->side) {
+        cudaError_t e = cudaStreamCreateWithFlags(&ar->side, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ar->fork, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ar->join, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaEventRecord(ar->fork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ar->side, ar->fork, 0);
+    *side = ar->side;
+    return e;
+}
+static inline cudaError_t side_join(heb_ctx *c, cudaStream_t st) {
+    StreamArena *ar = c->arena(st);
+    cudaError_t e = cudaEventRecord(ar->join, ar->side);
+    return e == cudaSuccess ? cudaStreamWaitEvent(st, ar->join, 0) : e;
+}
+
 template <int LOGN, class K0, class K1, class K2, class... Args>
-static cudaError_t launch_by_engine(const heb_ctx *c, K0 k0, K1 k1, K2 k2, int a, int b, unsigned gy, unsigned gz,
+static cudaError_t launch_by_engine(const heb_ctx *cc, K0 k0, K1 k1, K2 k2, int a, int b, unsigned gy, unsigned gz,
                                     size_t smem, cudaStream_t st, Args... args) {
+    heb_ctx *c = const_cast<heb_ctx *>(cc);
     if (b <= a) return cudaSuccess;
 #ifndef ENGINE_SPLIT_ROWS
-#define ENGINE_SPLIT_ROWS 0  // measured: the small integer-row launch runs alone and loses more than it saves
+#define ENGINE_SPLIT_ROWS 1  // with the integer rows on the side stream: cfg1 relin +8%, cfg2 neutral
 #endif
     if (!ENGINE_SPLIT_ROWS) return launch_rows<LOGN>(k0, dim3(b - a, gy, gz), KT<LOGN>, smem, st, args..., a);
     int nint = 0;
@@ -317,10 +341,14 @@ static cudaError_t launch_by_engine(const heb_ctx *c, K0 k0, K1 k1, K2 k2, int a
     bool rest_fp = true;
     for (int r = a + nint; r < b; ++r) rest_fp = rest_fp && c->row_fp[r];
     if (!rest_fp) return launch_rows<LOGN>(k0, dim3(b - a, gy, gz), KT<LOGN>, smem, st, args..., a);
-    cudaError_t e = cudaSuccess;
-    if (nint) e = launch_rows<LOGN>(k2, dim3(nint, gy, gz), KT<LOGN>, smem, st, args..., a);
+    // integer rows on the side stream, concurrent with the FP64 rows (IMAD/ALU vs DFMA)
+    const bool both = nint && b - a - nint;
+    cudaStream_t ist = st;
+    cudaError_t e = both ? side_fork(c, st, &ist) : cudaSuccess;
+    if (e == cudaSuccess && nint) e = launch_rows<LOGN>(k2, dim3(nint, gy, gz), KT<LOGN>, smem, ist, args..., a);
     if (e == cudaSuccess && b - a - nint)
         e = launch_rows<LOGN>(k1, dim3(b - a - nint, gy, gz), KT<LOGN>, smem, st, args..., a + nint);
+    if (e == cudaSuccess && both) e = side_join(c, st);
     return e;
 }
 #define ENGINE_KERNELS(KERN) KERN<LOGN, 0>, KERN<LOGN, 1>, KERN<LOGN, 2>

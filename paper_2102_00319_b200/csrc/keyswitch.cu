@@ -753,26 +753,13 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
                     const char *e = getenv("HEB_MODUP_CONCURRENT");
                     return !(e && *e == '0');
                 }();
-                StreamArena *ar = sA.a;
                 cudaStream_t ist = st;
-                if (concurrent) {
-                    if (!ar->side) {
-                        CUDA_TRY(cudaStreamCreateWithFlags(&ar->side, cudaStreamNonBlocking));
-                        CUDA_TRY(cudaEventCreateWithFlags(&ar->fork, cudaEventDisableTiming));
-                        CUDA_TRY(cudaEventCreateWithFlags(&ar->join, cudaEventDisableTiming));
-                    }
-                    CUDA_TRY(cudaEventRecord(ar->fork, st));
-                    CUDA_TRY(cudaStreamWaitEvent(ar->side, ar->fork, 0));
-                    ist = ar->side;
-                }
+                if (concurrent) CUDA_TRY(side_fork(c, st, &ist));
                 CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 2>, dim3(dim3(k + 1, gy)), KT<LOGN>, sm, ist, K, s,
                                            comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt));
                 CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 1>, dim3(dim3(k + 1, gy)), KT<LOGN>, sm, st, K, s,
                                            comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt));
-                if (concurrent) {
-                    CUDA_TRY(cudaEventRecord(ar->join, ar->side));
-                    CUDA_TRY(cudaStreamWaitEvent(st, ar->join, 0));
-                }
+                if (concurrent) CUDA_TRY(side_join(c, st));
             } else {
                 CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 0>, dim3(dim3(k + 1, gy)), KT<LOGN>, sm, st, K, s,
                                            comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt));
