@@ -200,15 +200,26 @@ __device__ __forceinline__ void conv_body_limbs(double *wl, const Ctx &K, const 
     const int nf = min(FGF, F - f0);
     const int taps = C * P * Q;
     const int64_t roff = ((int64_t)r << logn) + x;
-    for (int e = w; e < taps * nf; e += SF) {
-        const int tap = e / nf, fl = e % nf;
-        const u64 *src = B.data + ((int64_t)(f0 + fl) * taps + tap) * B.ct_stride + roff;
-        const u64 b0 = src[0], b1 = src[B.comp_stride];
+    // weight limbs of the FGF filter slots (zero for slots past the last filter, so the
+    // hot loop needs no per-filter guard), and every tap's input offset
+    __shared__ int64_t toff[FP_MAX_TAPS];
+    for (int e = w; e < taps * FGF; e += SF) {
+        const int tap = e / FGF, fl = e % FGF;
         double *dst = wl + (size_t)(tap * FGF + fl) * 4 * XF + xl;
-        dst[0] = ntt::u2d(b0 >> 20);
-        dst[XF] = ntt::u2d(b0 & M20);
-        dst[2 * XF] = ntt::u2d(b1 >> 20);
-        dst[3 * XF] = ntt::u2d(b1 & M20);
+        if (fl < nf) {
+            const u64 *src = B.data + ((int64_t)(f0 + fl) * taps + tap) * B.ct_stride + roff;
+            const u64 b0 = src[0], b1 = src[B.comp_stride];
+            dst[0] = ntt::u2d(b0 >> 20);
+            dst[XF] = ntt::u2d(b0 & M20);
+            dst[2 * XF] = ntt::u2d(b1 >> 20);
+            dst[3 * XF] = ntt::u2d(b1 & M20);
+        } else {
+            dst[0] = dst[XF] = dst[2 * XF] = dst[3 * XF] = 0.0;
+        }
+    }
+    for (int tap = threadIdx.x; tap < taps; tap += blockDim.x) {
+        const int c = tap / (P * Q), pp = (tap / Q) % P, qq = tap % Q;
+        toff[tap] = ((int64_t)c * m * n + (int64_t)pp * n + qq) * A.ct_stride;
     }
     __syncthreads();
     const double pd = Pr.pd, pinvd = Pr.pinvd;
@@ -224,20 +235,12 @@ __device__ __forceinline__ void conv_body_limbs(double *wl, const Ctx &K, const 
         for (int fl = 0; fl < FGF; ++fl) h0[fl] = q0[fl] = l0[fl] = h1[fl] = q1[fl] = l1[fl] = h2[fl] = q2[fl] = l2[fl] = 0.0;
         // taps in (c, p, q) order; the next tap's inputs are loaded before this tap's math
         const u64 *base = A.data + ((int64_t)(i * s) * n + j * s) * A.ct_stride + roff;
-        int c = 0, pp = 0, qq = 0;
         u64 na0 = __ldg(base), na1 = __ldg(base + A.comp_stride);
         for (int tap = 0; tap < taps; ++tap) {
             {
                 const u64 a0 = na0, a1 = na1;
-                if (++qq == Q) {
-                    qq = 0;
-                    if (++pp == P) {
-                        pp = 0;
-                        ++c;
-                    }
-                }
                 if (tap + 1 < taps) {
-                    const u64 *ap = base + ((int64_t)c * m * n + (int64_t)pp * n + qq) * A.ct_stride;
+                    const u64 *ap = base + toff[tap + 1];
                     na0 = __ldg(ap);
                     na1 = __ldg(ap + A.comp_stride);
                 }
@@ -248,7 +251,7 @@ __device__ __forceinline__ void conv_body_limbs(double *wl, const Ctx &K, const 
                     const double *wt = wl + (size_t)(tap * FGF) * 4 * XF + xl;
 #pragma unroll
                     for (int fl = 0; fl < FGF; ++fl) {
-                        if (fl < nf) {
+                        {  // every slot: zero weights past the last filter
                             const double b0h = wt[(4 * fl) * XF], b0l = wt[(4 * fl + 1) * XF];
                             const double b1h = wt[(4 * fl + 2) * XF], b1l = wt[(4 * fl + 3) * XF];
                             const double bsh = b0h + b1h, bsl = b0l + b1l;
