@@ -181,13 +181,15 @@ __device__ __forceinline__ void conv_body(u64 *wsm, const Ctx &K, const heb_ct &
 // modular product plus an add; the three partial sums of each component are reduced
 // once per output cell.  Bounds: limbs of the component sums < 2^21, so every term is
 // < 2^42 and a sum of `taps` terms stays below 2^53 for taps <= 256.  The weight limbs
-// are staged in shared memory as doubles ([tap][filter][b0h, b0l, b1h, b1l][XF]).
+// and their Karatsuba sums are staged in shared memory as double pairs
+// ([tap][filter][(b0h, b0l), (b1h, b1l), (b0h + b1h, b0l + b1l)][XF]).
 namespace {
 constexpr int XF = 16;  // positions per CTA
 constexpr int SF = 16;  // workers per position -> 256 threads
 constexpr int FGF = CONV_FGF;  // filters per CTA group
 constexpr int FP_MAX_TAPS = 256;
 constexpr u64 M20 = (1ull << 20) - 1;
+constexpr int WPAIRS = 3;  // staged weight double2 per (tap, filter)
 }  // namespace
 
 __device__ __forceinline__ void conv_body_limbs(double *wl, const Ctx &K, const heb_ct &A, const heb_ct &B,
@@ -205,16 +207,18 @@ __device__ __forceinline__ void conv_body_limbs(double *wl, const Ctx &K, const 
     __shared__ int64_t toff[FP_MAX_TAPS];
     for (int e = w; e < taps * FGF; e += SF) {
         const int tap = e / FGF, fl = e % FGF;
-        double *dst = wl + (size_t)(tap * FGF + fl) * 4 * XF + xl;
+        // [tap][filter][pair][XF] double2: (b0h, b0l), (b1h, b1l), (b0h + b1h, b0l + b1l)
+        double2 *dst = reinterpret_cast<double2 *>(wl) + (size_t)(tap * FGF + fl) * WPAIRS * XF + xl;
         if (fl < nf) {
             const u64 *src = B.data + ((int64_t)(f0 + fl) * taps + tap) * B.ct_stride + roff;
             const u64 b0 = src[0], b1 = src[B.comp_stride];
-            dst[0] = ntt::u2d(b0 >> 20);
-            dst[XF] = ntt::u2d(b0 & M20);
-            dst[2 * XF] = ntt::u2d(b1 >> 20);
-            dst[3 * XF] = ntt::u2d(b1 & M20);
+            const double b0h = ntt::u2d(b0 >> 20), b0l = ntt::u2d(b0 & M20);
+            const double b1h = ntt::u2d(b1 >> 20), b1l = ntt::u2d(b1 & M20);
+            dst[0] = make_double2(b0h, b0l);
+            dst[XF] = make_double2(b1h, b1l);
+            dst[2 * XF] = make_double2(b0h + b1h, b0l + b1l);
         } else {
-            dst[0] = dst[XF] = dst[2 * XF] = dst[3 * XF] = 0.0;
+            dst[0] = dst[XF] = dst[2 * XF] = make_double2(0.0, 0.0);
         }
     }
     for (int tap = threadIdx.x; tap < taps; tap += blockDim.x) {
@@ -248,13 +252,13 @@ __device__ __forceinline__ void conv_body_limbs(double *wl, const Ctx &K, const 
                     const double a0h = ntt::u2d(a0 >> 20), a0l = ntt::u2d(a0 & M20);
                     const double a1h = ntt::u2d(a1 >> 20), a1l = ntt::u2d(a1 & M20);
                     const double ash = a0h + a1h, asl = a0l + a1l;
-                    const double *wt = wl + (size_t)(tap * FGF) * 4 * XF + xl;
+                    const double2 *wt = reinterpret_cast<const double2 *>(wl) + (size_t)(tap * FGF) * WPAIRS * XF + xl;
 #pragma unroll
                     for (int fl = 0; fl < FGF; ++fl) {
                         {  // every slot: zero weights past the last filter
-                            const double b0h = wt[(4 * fl) * XF], b0l = wt[(4 * fl + 1) * XF];
-                            const double b1h = wt[(4 * fl + 2) * XF], b1l = wt[(4 * fl + 3) * XF];
-                            const double bsh = b0h + b1h, bsl = b0l + b1l;
+                            const double2 w0 = wt[(WPAIRS * fl) * XF], w1 = wt[(WPAIRS * fl + 1) * XF];
+                            const double2 ws = wt[(WPAIRS * fl + 2) * XF];
+                            const double b0h = w0.x, b0l = w0.y, b1h = w1.x, b1l = w1.y, bsh = ws.x, bsl = ws.y;
                             h0[fl] = fma(a0h, b0h, h0[fl]);
                             q0[fl] = fma(a0h, b0l, fma(a0l, b0h, q0[fl]));
                             l0[fl] = fma(a0l, b0l, l0[fl]);
@@ -337,8 +341,8 @@ extern "C" int heb_conv_tensor(heb_ctx *c, heb_ct a, heb_ct b, heb_ct d, int cha
     if (sm > 220 * 1024) return fail(HEB_EUNSUP, "heb_conv_tensor: %d taps exceed the shared-memory stage", taps);
     cudaStream_t st = (cudaStream_t)stream;
     const bool need_flush = taps > c->flush;
-    const bool limbs = taps <= FP_MAX_TAPS && !getenv_flag("HEB_CONV_NO_LIMBS");
-    const size_t smf = sizeof(double) * (size_t)taps * FGF * 4 * XF;
+    const size_t smf = sizeof(double2) * (size_t)taps * FGF * WPAIRS * XF;
+    const bool limbs = taps <= FP_MAX_TAPS && smf <= 200 * 1024 && !getenv_flag("HEB_CONV_NO_LIMBS");
     const size_t smem = limbs ? std::max(sm, smf) : sm;
     static_assert(FG == FGF, "both bodies use the same filter groups");
     ConvMap map{};
