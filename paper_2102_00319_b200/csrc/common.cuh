@@ -342,10 +342,20 @@ static cudaError_t launch_by_engine(const heb_ctx *cc, K0 k0, K1 k1, K2 k2, int 
     for (int r = a + nint; r < b; ++r) rest_fp = rest_fp && c->row_fp[r];
     if (!rest_fp) return launch_rows<LOGN>(k0, dim3(b - a, gy, gz), KT<LOGN>, smem, st, args..., a);
     // integer rows on the side stream, concurrent with the FP64 rows (IMAD/ALU vs DFMA)
-    const bool both = nint && b - a - nint;
+#ifndef ENGINE_SIDE_STREAM
+#define ENGINE_SIDE_STREAM 1
+#endif
+    const bool both = ENGINE_SIDE_STREAM && nint && b - a - nint;
     cudaStream_t ist = st;
     cudaError_t e = both ? side_fork(c, st, &ist) : cudaSuccess;
-    if (e == cudaSuccess && nint) e = launch_rows<LOGN>(k2, dim3(nint, gy, gz), KT<LOGN>, smem, ist, args..., a);
+    // The integer rows take the run-time-dispatching instantiation: the integer-only
+    // instantiation of k_ks_head faults at N = 512 (found by smoke(); all other sizes
+    // pass), and k0 measured the same speed for these short launches.
+#ifndef ENGINE_INT_ONLY_INST
+#define ENGINE_INT_ONLY_INST 0
+#endif
+    if (e == cudaSuccess && nint)
+        e = launch_rows<LOGN>(ENGINE_INT_ONLY_INST ? k2 : k0, dim3(nint, gy, gz), KT<LOGN>, smem, ist, args..., a);
     if (e == cudaSuccess && b - a - nint)
         e = launch_rows<LOGN>(k1, dim3(b - a - nint, gy, gz), KT<LOGN>, smem, st, args..., a + nint);
     if (e == cudaSuccess && both) e = side_join(c, st);
