@@ -408,7 +408,7 @@ class LayerEvaluator:
             with torch.cuda.stream(st):
                 self.run(enc, x)  # builds index caches / kernel attributes outside the capture
             st.synchronize()
-            graph = torch.cuda.CUDAGraph()
+            graph = torch.cuda.CUDAGraph(keep_graph=True)  # raw graph kept for graph_kernel_launches
             before = self.be.counters.snapshot().__dict__
             with torch.cuda.graph(graph, pool=torch.cuda.graph_pool_handle(), stream=st,
                                   capture_error_mode="thread_local"):
@@ -417,8 +417,26 @@ class LayerEvaluator:
             delta = {f: after[f] - before[f] for f in after}
             # warm-up and capture are not user-visible evaluations: take their tallies back
             self.be.counters.bump(**{f: start[f] - after[f] for f in after})
+            graph.instantiate()
             hit = self._graphs[key] = (graph, out, delta, enc, x.buf)  # keep the captured buffers alive
         return hit[:3]
+
+    def graph_kernel_launches(self, enc: EncryptedNetworkBatch, x: CipherBatch, pipeline: int = 0) -> int:
+        """Kernel nodes of the captured CUDA graph of one inference (= kernel launches per
+        replayed step; every kernel in it is launched by libheb200)."""
+        from cuda.bindings import runtime as rt
+
+        graph = self.captured(enc, x, pipeline)[0]
+        g = graph.raw_cuda_graph()
+        err, _, count = rt.cudaGraphGetNodes(g, 0)
+        err, nodes, count = rt.cudaGraphGetNodes(g, count)
+        if err != rt.cudaError_t.cudaSuccess:
+            raise RuntimeError(f"cudaGraphGetNodes: {err}")
+        kernels = 0
+        for nd in nodes[:count]:
+            err, kind = rt.cudaGraphNodeGetType(nd)
+            kernels += int(kind == rt.cudaGraphNodeType.cudaGraphNodeTypeKernel)
+        return kernels
 
     def _replay(self, runner) -> CipherBatch:
         graph, out, delta = runner
