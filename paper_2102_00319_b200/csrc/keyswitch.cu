@@ -618,24 +618,30 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_down_rescale_tail(Ctx K, const u64 *acc, h
         const double ar = (double)Ci.alpha_r.x, br = (double)Ci.beta_r.x;
         const double ar32 = (double)ntt::fcanon(ntt::fmul(4294967296.0, ar, pd, pinvd), pd, pinvd);
         const double al = (double)Ci.alpha.x, be = (double)Ci.beta.x;
+        // the transform takes and returns raw doubles (|v| < 2^47, FpArithRawIO): no
+        // canonicalise / convert round trip on either side of it
+        const ntt::FpArithRawIO fa(pd, pinvd);
+        double *s2 = reinterpret_cast<double *>(sm);
+        const double *twf = K.twf + ((size_t)i << LOGN);
         for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
             const i64 *ap = aP + (b * 2 + c) * n;
             const i64 *cl = cL + (b * 2 + c) * n;
             u64 y[16];
-            fwd_any<LOGN, 16, ENG>(K, i, Pi, sm,
-                          [&](int j) {
-                              const double v = fp_imul(__ldcg(ap + j), ar, ar32, pd, pinvd) +
-                                               ntt::fmul((double)__ldcg(cl + j), br, pd, pinvd);
-                              return ntt::fcanon(v, pd, pinvd);
-                          },
-                          y);
+            auto ld = [&](int j) -> u64 {
+                const double v = fp_imul(__ldcg(ap + j), ar, ar32, pd, pinvd) +
+                                 ntt::fmul((double)__ldcg(cl + j), br, pd, pinvd);
+                return (u64)__double_as_longlong(v);
+            };
+            constexpr int LL = Row<LOGN>::LL;
+            if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, 16>(fa, s2, twf, ld, y, rhalf<LOGN>());
+            else ntt::forward<LL, 16>(fa, s2, twf, ld, y);
             u64 x[16], z[16];
             load16<LOGN>(acc + ((b * 2 + c) * (k + 1) + i) * n + pos, x);
             load16<LOGN>(at(d, b, c, i, LOGN) + pos, z);
 #pragma unroll
             for (int m = 0; m < 16; ++m)
                 x[m] = ntt::fcanon(ntt::fmul(ntt::u2d(x[m]), al, pd, pinvd) + ntt::fmul(ntt::u2d(z[m]), be, pd, pinvd) -
-                                       ntt::u2d(y[m]),
+                                       __longlong_as_double((long long)y[m]),
                                    pd, pinvd);
             store16<LOGN>(at(out, b, c, i, LOGN) + pos, x);
         }

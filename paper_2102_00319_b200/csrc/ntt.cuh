@@ -163,6 +163,11 @@ struct FpArithRaw : FpArith {
     HD FpArithRaw(double p_, double pinv_) : FpArith(p_, pinv_) {}
     HD u64 out_fwd(V x) const { return (u64)__double_as_longlong(x); }
 };
+// ... and whose forward also takes raw doubles (bit patterns, |v| < 2^47) as input
+struct FpArithRawIO : FpArithRaw {
+    HD FpArithRawIO(double p_, double pinv_) : FpArithRaw(p_, pinv_) {}
+    HD V in(u64 x) const { return __longlong_as_double((long long)x); }
+};
 
 // ---------------------------------------------------------------- forward ----
 // One forward group: radix 2^RB covering stages S0 .. S0+RB-1.
