@@ -101,6 +101,11 @@ int heb_tensor(heb_ctx *ctx, heb_ct a, heb_ct b, heb_ct raw, int64_t count, int 
  * plaintext rows (mul_ct_pt = mul_rows + rescale, ckks.py:320-331). */
 int heb_rescale(heb_ctx *ctx, heb_ct in, const uint64_t *pt, int64_t pt_stride, heb_ct out, int64_t count,
                 int comps, int level, void *stream);
+/* mul_ct_pt (ckks.py:320-331, base.py:427-445): both components times the plaintext
+ * rows (pt: level+1 rows, item stride pt_stride; 0 = broadcast), then rescale to
+ * level-1.  Same as heb_rescale with pt != NULL and comps = 2. */
+int heb_mul_plain_rescale(heb_ctx *ctx, heb_ct ct, const uint64_t *pt, int64_t pt_stride, heb_ct out, int64_t count,
+                          int level, void *stream);
 /* Prepare a switching key for the device key switch: from the reference layout
  * (EvalKeyPayload b/a arrays, (digits, num_rows, N) Montgomery residues, ckks.py:72-75)
  * to (digits, num_rows, 2, N) pairs (w, floor(w*2^64/p)) with w = residue * R^-1, so

@@ -51,6 +51,7 @@ SIGNATURES: dict[str, list] = {
     "heb_add_plain": [_P, _CT, _P, _L, _CT, _L, _I, _P],
     "heb_tensor": [_P, _CT, _CT, _CT, _L, _I, _I, _P],
     "heb_rescale": [_P, _CT, _P, _L, _CT, _L, _I, _I, _P],
+    "heb_mul_plain_rescale": [_P, _CT, _P, _L, _CT, _L, _I, _P],
     "heb_prepare_switch_key": [_P, _P, _P, _I, _P, _P],
     "heb_relin_rescale": [_P, _CT, _P, _CT, _L, _I, _P],
     "heb_rotate": [_P, _CT, _P, _CT, _L, _I, _U, _P],

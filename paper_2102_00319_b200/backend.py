@@ -372,8 +372,8 @@ class B200Backend(HEBackend):
     def _mul_ct_pt_impl(self, ct, plain) -> DevCipher:
         k = ct.level + 1
         out = self.ctx.empty(2, k - 1, self.n)
-        self.ctx.call("heb_rescale", ct_desc(ct.payload.buf), plain.payload.rows.data_ptr(), 0, ct_desc(out), 1, 2,
-                      ct.level, self.ctx.stream)
+        self.ctx.call("heb_mul_plain_rescale", ct_desc(ct.payload.buf), plain.payload.rows.data_ptr(), 0,
+                      ct_desc(out), 1, ct.level, self.ctx.stream)
         return DevCipher(out, k - 1)
 
     def _mul_raw_impl(self, a, b) -> DevRaw:

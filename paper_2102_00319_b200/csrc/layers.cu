@@ -90,6 +90,13 @@ static int add_bias(heb_ctx *c, heb_ct y, heb_ct bias, int64_t count, int64_t pe
     return HEB_OK;
 }
 
+// mul_ct_pt (ckks.py:320-331): product with the plaintext rows fused into the rescale
+extern "C" int heb_mul_plain_rescale(heb_ctx *c, heb_ct ct, const uint64_t *pt, int64_t pt_stride, heb_ct out,
+                                     int64_t count, int level, void *stream) {
+    if (!pt) return fail(HEB_EINVAL, "heb_mul_plain_rescale: null plaintext");
+    return heb_rescale(c, ct, pt, pt_stride, out, count, 2, level, stream);
+}
+
 extern "C" int heb_conv(heb_ctx *c, heb_ct x, heb_ct w, heb_ct bias, heb_ct out, int channels, int m, int n,
                         int filters, int kp, int kq, int stride, int level, const uint64_t *evk, void *stream) {
     if (!c || !evk || channels < 1 || filters < 1 || kp < 1 || kq < 1 || stride < 1 || kp > m || kq > n ||

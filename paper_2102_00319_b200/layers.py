@@ -232,8 +232,8 @@ class LayerEvaluator:
     def mul_plain(self, y: CipherBatch, pt, values_mag: float) -> CipherBatch:
         meta = self._mul_plain_meta(y.level, y.scale, y.noise_bits, pt, values_mag)
         out = self._empty(y.count, 2, y.level)
-        self.ctx.call("heb_rescale", y.desc(), pt.payload.rows.data_ptr(), 0, ct_desc(out), y.count, 2, y.level,
-                      self.ctx.stream)
+        self.ctx.call("heb_mul_plain_rescale", y.desc(), pt.payload.rows.data_ptr(), 0, ct_desc(out), y.count,
+                      y.level, self.ctx.stream)
         self.be.counters.bump(ctpt_mult=y.count)
         return CipherBatch(out, *meta)
 
