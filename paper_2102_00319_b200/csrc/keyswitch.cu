@@ -534,9 +534,9 @@ extern "C" int heb_prepare_switch_key(heb_ctx *c, const uint64_t *kb, const uint
 // which = 0: aP = center_P(INTT_P(acc_P)) ; which = 1: bL = INTT_L(acc_L + P d_L) (std form)
 template <int LOGN, int ENG>
 __global__ void ROW_BOUNDS(LOGN) k_ks_down_head(Ctx K, const u64 *acc, heb_ct d, int k,
-                                                                        i64 *aP, u64 *bL, int64_t count) {
+                                                                        i64 *aP, u64 *bL, int64_t count, int which0) {
     extern __shared__ u64 sm[];
-    const int which = lbx<LOGN>(), c = blockIdx.z;
+    const int which = which0 + lbx<LOGN>(), c = blockIdx.z;
     const int n = 1 << LOGN;
     const int pos = tpos<LOGN>();
     const int row = which == 0 ? K.num_rows - 1 : k - 1;
@@ -598,6 +598,21 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_down_head_cl(Ctx K, const u64 *acc, heb_ct
                           cl[i] = center(sl, PL.p);
                       },
                       true);
+    }
+}
+
+// cL = center((bL - aP) P^-1 mod q_L) elementwise, from bL = INTT_L(acc_L + P d_L) (std
+// form, k_ks_down_head which = 1) and aP: the same values k_ks_down_head_cl produces,
+// with the two transforms run concurrently (integer P row / FP64 q_L row) before it.
+__global__ void k_cl_combine(Ctx K, const u64 *__restrict__ bL, const i64 *__restrict__ aP, int k, i64 *cL,
+                             int64_t total) {
+    const int L = k - 1;
+    const PrimeInfo PL = K.pi[L];
+    const LevelConst C = K.lc[(size_t)L * K.num_rows + L];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const u64 sl = sub_mod(shoup(__ldcs(bL + i), C.pinv.x, C.pinv.y, PL.p),
+                               signed_mul_const(__ldcs(aP + i), C.pinv.x, C.pinv.y, PL.p), PL.p);
+        cL[i] = center(sl, PL.p);
     }
 }
 
@@ -729,11 +744,12 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
     }();
     // TMEM accesses are warp-wide: rows of fewer than 32 x 16 residues per CTA take the split path
     const bool fused = fused_env && KT<LOGN> % 32 == 0;
-    Scratch sD(c, st), sA(c, st), sP(c, st), sL(c, st), sV(c, st);
+    Scratch sD(c, st), sA(c, st), sP(c, st), sL(c, st), sB(c, st), sV(c, st);
     CUDA_TRY(sD.get(sizeof(i64) * (size_t)cmax * k * n));
     CUDA_TRY(sA.get(sizeof(u64) * (size_t)cmax * 2 * (k + 1) * n));
     CUDA_TRY(sP.get(sizeof(i64) * (size_t)cmax * 2 * n));
     CUDA_TRY(sL.get(sizeof(u64) * (size_t)cmax * 2 * n));
+    CUDA_TRY(sB.get(rescale ? sizeof(u64) * (size_t)cmax * 2 * n : 256));
     CUDA_TRY(sV.get(fused ? 256 : sizeof(u64) * (size_t)sub * (k + 1) * k * n));
     const Ctx K = kctx(c);
     for (int64_t b0 = 0; b0 < count; b0 += chunk) {
@@ -791,11 +807,41 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
             LAUNCH_CHECK();
         }
         if (rescale) {
-            { PROF("k_ks_down_head", st, 8.0 * n * cnt * 4.0); CUDA_TRY(launch_rows<LOGN>(c->row_fp[c->num_rows - 1] ? k_ks_down_head<LOGN, 1> : k_ks_down_head<LOGN, 2>, dim3(dim3(1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
-                                                                 (u64 *)nullptr, cnt)); }
+            // aP = center(INTT_P(acc_P)) (special prime) and bL = INTT_L(acc_L + P d_L) are
+            // independent: the P transform goes to the side stream, then one elementwise
+            // pass forms cL (HEB_MODDOWN_CONCURRENT=0: the sequential k_ks_down_head_cl)
+            static const bool conc = [] {
+                const char *e = getenv("HEB_MODDOWN_CONCURRENT");
+                return !(e && *e == '0');
+            }();
+            auto head_p = c->row_fp[c->num_rows - 1] ? k_ks_down_head<LOGN, 1> : k_ks_down_head<LOGN, 2>;
+            if (conc) {
+                PROF("k_ks_down_head", st, 8.0 * n * cnt * 2.0 * 2.0 * 2.0);
+                cudaStream_t side;
+                CUDA_TRY(side_fork(c, st, &side));
+                CUDA_TRY(launch_rows<LOGN>(head_p, dim3(dim3(1, gy, 2)), KT<LOGN>, sm, side, K, (const u64 *)sA.p, dd, k,
+                                           (i64 *)sP.p, (u64 *)nullptr, cnt, 0));
+                CUDA_TRY(launch_rows<LOGN>(c->row_fp[k - 1] ? k_ks_down_head<LOGN, 1> : k_ks_down_head<LOGN, 2>,
+                                           dim3(dim3(1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd, k,
+                                           (i64 *)nullptr, (u64 *)sB.p, cnt, 1));
+                CUDA_TRY(side_join(c, st));
+            } else {
+                PROF("k_ks_down_head", st, 8.0 * n * cnt * 4.0);
+                CUDA_TRY(launch_rows<LOGN>(head_p, dim3(dim3(1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd, k,
+                                           (i64 *)sP.p, (u64 *)nullptr, cnt, 0));
+            }
             LAUNCH_CHECK();
-            { PROF("k_ks_down_head_cl", st, 8.0 * n * cnt * 2.0 * 4.0); CUDA_TRY(launch_rows<LOGN>(c->row_fp[k - 1] ? k_ks_down_head_cl<LOGN, 1> : k_ks_down_head_cl<LOGN, 2>, dim3(dim3(1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd, k, (const i64 *)sP.p,
-                                                                 (i64 *)sL.p, cnt)); }
+            if (conc) {
+                PROF("k_cl_combine", st, 8.0 * n * cnt * 2.0 * 3.0);
+                const int64_t total = cnt * 2 * n;
+                k_cl_combine<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(
+                    K, (const u64 *)sB.p, (const i64 *)sP.p, k, (i64 *)sL.p, total);
+            } else {
+                PROF("k_ks_down_head_cl", st, 8.0 * n * cnt * 2.0 * 4.0);
+                CUDA_TRY(launch_rows<LOGN>(c->row_fp[k - 1] ? k_ks_down_head_cl<LOGN, 1> : k_ks_down_head_cl<LOGN, 2>,
+                                           dim3(dim3(1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd, k,
+                                           (const i64 *)sP.p, (i64 *)sL.p, cnt));
+            }
             LAUNCH_CHECK();
             { PROF("k_ks_down_rescale_tail", st, 8.0 * n * cnt * 2.0 * (2 + 3 * (k - 1))); CUDA_TRY(launch_by_engine<LOGN>(c, ENGINE_KERNELS(k_ks_down_rescale_tail), 0, k - 1, gy, 2, sm, st, K, (const u64 *)sA.p, dd,
                                                                              (const i64 *)sP.p, (const i64 *)sL.p, k,
@@ -803,7 +849,7 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
             LAUNCH_CHECK();
         } else {
             { PROF("k_ks_down_head", st, 8.0 * n * cnt * 4.0); CUDA_TRY(launch_rows<LOGN>(c->row_fp[c->num_rows - 1] ? k_ks_down_head<LOGN, 1> : k_ks_down_head<LOGN, 2>, dim3(dim3(1, gy, 2)), KT<LOGN>, sm, st, K, (const u64 *)sA.p, dd, k, (i64 *)sP.p,
-                                                                 (u64 *)sL.p, cnt)); }
+                                                                 (u64 *)sL.p, cnt, 0)); }
             LAUNCH_CHECK();
             { PROF("k_ks_down_tail", st, 8.0 * n * cnt * (2.0 + 5.0 * k)); CUDA_TRY(launch_by_engine<LOGN>(c, ENGINE_KERNELS(k_ks_down_tail), 0, k, gy, 2, sm, st, K, (const u64 *)sA.p, (const i64 *)sP.p, k, dd, o,
                                                                  cnt)); }
