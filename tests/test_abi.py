@@ -17,6 +17,19 @@ def test_header_declares_entry_points():
     assert len(names) >= 25
 
 
+# SURVEY.md 8(b) "minimum C-ABI exports" (names as the survey gives them)
+SURVEY_8B = ["heb_ctx_create", "heb_ctx_destroy", "heb_alloc", "heb_free", "heb_h2d", "heb_d2h", "heb_ntt_fwd",
+             "heb_ntt_inv", "heb_add", "heb_add_plain", "heb_tensor", "heb_mul_plain_rescale", "heb_rescale",
+             "heb_relin_rescale", "heb_rotate", "heb_conv", "heb_square", "heb_poly_act", "heb_sumpool", "heb_fc",
+             "heb_gather_logits", "heb_last_error"]
+
+
+def test_header_covers_survey_boundary():
+    names = set(_header_functions())
+    missing = [n for n in SURVEY_8B if n not in names]
+    assert not missing, missing
+
+
 def test_library_exports_every_declared_symbol():
     from paper_2102_00319_b200 import _lib
     from paper_2102_00319_b200.build import build
