@@ -55,7 +55,16 @@ __global__ void k_pack_rows(const u64 *__restrict__ in, int64_t in_stride, u64 *
     }
 }
 
-// one thread per residue: reads the one or two words holding it
+// one thread per residue pair: reads the (at most three) words holding them, one
+// 16-byte streaming store
+__device__ __forceinline__ u64 unpack_one(const u64 *__restrict__ src, int64_t i, int b, u64 mask) {
+    const int64_t o = i * b;
+    const int64_t w = o >> 6;
+    const int s = (int)(o & 63);
+    u64 v = __ldg(src + w) >> s;
+    if (s + b > 64) v |= __ldg(src + w + 1) << (64 - s);
+    return v & mask;
+}
 __global__ void k_unpack_rows(const u64 *__restrict__ in, u64 *__restrict__ out, int64_t out_stride, PackGeom g,
                               int rows, int logn, int64_t count) {
     const int r = blockIdx.y;
@@ -64,15 +73,9 @@ __global__ void k_unpack_rows(const u64 *__restrict__ in, u64 *__restrict__ out,
     const u64 mask = b == 64 ? ~0ull : ((1ull << b) - 1);
     for (int64_t blk = blockIdx.z; blk < count; blk += gridDim.z) {
         const u64 *src = in + blk * g.off[rows] + g.off[r];
-        u64 *dst = out + blk * out_stride + ((int64_t)r << logn);
-        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-            const int64_t o = (int64_t)i * b;
-            const int64_t w = o >> 6;
-            const int s = (int)(o & 63);
-            u64 v = __ldg(src + w) >> s;
-            if (s + b > 64) v |= __ldg(src + w + 1) << (64 - s);
-            __stcs(dst + i, v & mask);
-        }
+        ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(out + blk * out_stride + ((int64_t)r << logn));
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n / 2; i += gridDim.x * blockDim.x)
+            __stcs(dst + i, make_ulonglong2(unpack_one(src, 2 * i, b, mask), unpack_one(src, 2 * i + 1, b, mask)));
     }
 }
 
@@ -103,7 +106,8 @@ extern "C" int heb_unpack_rows(heb_ctx *c, const uint64_t *in, int64_t count, in
         return fail(HEB_EINVAL, "heb_unpack_rows: bad args");
     if (count <= 0) return HEB_OK;
     const PackGeom g = geometry(c, rows);
-    const dim3 grid((unsigned)((c->n + 255) / 256), rows, gdim(count));
+    if (out_stride & 1) return fail(HEB_EINVAL, "heb_unpack_rows: odd output stride");
+    const dim3 grid((unsigned)((c->n / 2 + 255) / 256), rows, gdim(count));
     {
         PROF("k_unpack_rows", (cudaStream_t)stream, 8.0 * (double)count * ((double)rows * c->n + g.off[rows]));
         k_unpack_rows<<<grid, 256, 0, (cudaStream_t)stream>>>(in, out, out_stride, g, rows, c->log_n, count);
