@@ -29,31 +29,42 @@ __global__ void k_add_plain(Ctx K, heb_ct a, const u64 *pt, int64_t pstride, heb
     }
 }
 
-// (d0, d1, d2) (+)= (a0 b0, a0 b1 + a1 b0, a1 b1); d1 via Karatsuba (3 products)
+// (d0, d1, d2) (+)= (a0 b0, a0 b1 + a1 b0, a1 b1); d1 via Karatsuba (3 products).
+// Two adjacent positions per thread (16-byte loads and stores).
+__device__ __forceinline__ void tensor_one(u64 x0, u64 x1, u64 y0, u64 y1, const PrimeInfo &P, unsigned long long &e0, unsigned long long &e1,
+                                           unsigned long long &e2) {
+    e0 = mont_mul(x0, y0, P.p, P.pinv);
+    e2 = mont_mul(x1, y1, P.p, P.pinv);
+    const u64 s = mont_mul(add_mod(x0, x1, P.p), add_mod(y0, y1, P.p), P.p, P.pinv);
+    e1 = sub_mod(sub_mod(s, e0, P.p), e2, P.p);
+}
 __global__ void k_tensor(Ctx K, heb_ct a, heb_ct b, heb_ct d, int64_t lines, int k, int logn, int acc) {
     const int n = 1 << logn;
     for (int64_t line = blockIdx.y; line < lines; line += gridDim.y) {
         const int r = (int)(line % k);
         const int64_t it = line / k;
         const PrimeInfo P = K.pi[r];
-        const u64 *a0 = at(a, it, 0, r, logn), *a1 = at(a, it, 1, r, logn);
-        const u64 *b0 = at(b, it, 0, r, logn), *b1 = at(b, it, 1, r, logn);
-        u64 *d0 = at(d, it, 0, r, logn), *d1 = at(d, it, 1, r, logn), *d2 = at(d, it, 2, r, logn);
-        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-            const u64 x0 = a0[i], x1 = a1[i], y0 = b0[i], y1 = b1[i];
-            const u64 e0 = mont_mul(x0, y0, P.p, P.pinv);
-            const u64 e2 = mont_mul(x1, y1, P.p, P.pinv);
-            const u64 s = mont_mul(add_mod(x0, x1, P.p), add_mod(y0, y1, P.p), P.p, P.pinv);
-            const u64 e1 = sub_mod(sub_mod(s, e0, P.p), e2, P.p);
+        const ulonglong2 *a0 = reinterpret_cast<const ulonglong2 *>(at(a, it, 0, r, logn));
+        const ulonglong2 *a1 = reinterpret_cast<const ulonglong2 *>(at(a, it, 1, r, logn));
+        const ulonglong2 *b0 = reinterpret_cast<const ulonglong2 *>(at(b, it, 0, r, logn));
+        const ulonglong2 *b1 = reinterpret_cast<const ulonglong2 *>(at(b, it, 1, r, logn));
+        ulonglong2 *d0 = reinterpret_cast<ulonglong2 *>(at(d, it, 0, r, logn));
+        ulonglong2 *d1 = reinterpret_cast<ulonglong2 *>(at(d, it, 1, r, logn));
+        ulonglong2 *d2 = reinterpret_cast<ulonglong2 *>(at(d, it, 2, r, logn));
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n / 2; i += gridDim.x * blockDim.x) {
+            const ulonglong2 x0 = a0[i], x1 = a1[i], y0 = b0[i], y1 = b1[i];
+            ulonglong2 e0, e1, e2;
+            tensor_one(x0.x, x1.x, y0.x, y1.x, P, e0.x, e1.x, e2.x);
+            tensor_one(x0.y, x1.y, y0.y, y1.y, P, e0.y, e1.y, e2.y);
             if (acc) {
-                d0[i] = add_mod(d0[i], e0, P.p);
-                d1[i] = add_mod(d1[i], e1, P.p);
-                d2[i] = add_mod(d2[i], e2, P.p);
-            } else {
-                d0[i] = e0;
-                d1[i] = e1;
-                d2[i] = e2;
+                const ulonglong2 o0 = d0[i], o1 = d1[i], o2 = d2[i];
+                e0 = make_ulonglong2(add_mod(o0.x, e0.x, P.p), add_mod(o0.y, e0.y, P.p));
+                e1 = make_ulonglong2(add_mod(o1.x, e1.x, P.p), add_mod(o1.y, e1.y, P.p));
+                e2 = make_ulonglong2(add_mod(o2.x, e2.x, P.p), add_mod(o2.y, e2.y, P.p));
             }
+            d0[i] = e0;
+            d1[i] = e1;
+            d2[i] = e2;
         }
     }
 }
@@ -112,9 +123,11 @@ extern "C" int heb_add_plain(heb_ctx *c, heb_ct a, const uint64_t *pt, int64_t p
 extern "C" int heb_tensor(heb_ctx *c, heb_ct a, heb_ct b, heb_ct d, int64_t count, int k, int accumulate,
                           void *stream) {
     if (!c || k < 1 || k > c->num_rows) return fail(HEB_EINVAL, "heb_tensor: bad args");
+    if ((a.ct_stride | a.comp_stride | b.ct_stride | b.comp_stride | d.ct_stride | d.comp_stride) & 1)
+        return fail(HEB_EINVAL, "heb_tensor: strides must be even (16-byte position pairs)");
     if (count <= 0) return HEB_OK;
     const int64_t lines = count * k;
-    { PROF("k_tensor", (cudaStream_t)stream, 8.0 * c->n * lines * (accumulate ? 10.0 : 7.0)); k_tensor<<<pw_grid(c->n, lines), 256, 0, (cudaStream_t)stream>>>(kctx(c), a, b, d, lines, k, c->log_n,
+    { PROF("k_tensor", (cudaStream_t)stream, 8.0 * c->n * lines * (accumulate ? 10.0 : 7.0)); k_tensor<<<pw_grid(c->n / 2, lines), 256, 0, (cudaStream_t)stream>>>(kctx(c), a, b, d, lines, k, c->log_n,
                                                                       accumulate); }
     LAUNCH_CHECK();
     return HEB_OK;
