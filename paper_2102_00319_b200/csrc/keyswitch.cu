@@ -609,10 +609,18 @@ __global__ void k_cl_combine(Ctx K, const u64 *__restrict__ bL, const i64 *__res
     const int L = k - 1;
     const PrimeInfo PL = K.pi[L];
     const LevelConst C = K.lc[(size_t)L * K.num_rows + L];
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const u64 sl = sub_mod(shoup(__ldcs(bL + i), C.pinv.x, C.pinv.y, PL.p),
-                               signed_mul_const(__ldcs(aP + i), C.pinv.x, C.pinv.y, PL.p), PL.p);
-        cL[i] = center(sl, PL.p);
+    auto one = [&](u64 b, i64 a) {
+        return center(sub_mod(shoup(b, C.pinv.x, C.pinv.y, PL.p), signed_mul_const(a, C.pinv.x, C.pinv.y, PL.p), PL.p),
+                      PL.p);
+    };
+    // position pairs, 16-byte accesses (total is even: whole rows of N)
+    const ulonglong2 *b2 = reinterpret_cast<const ulonglong2 *>(bL);
+    const longlong2 *a2 = reinterpret_cast<const longlong2 *>(aP);
+    longlong2 *c2 = reinterpret_cast<longlong2 *>(cL);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total / 2; i += (int64_t)gridDim.x * blockDim.x) {
+        const ulonglong2 b = __ldcs(b2 + i);
+        const longlong2 a = __ldcs(a2 + i);
+        c2[i] = make_longlong2(one(b.x, a.x), one(b.y, a.y));
     }
 }
 
