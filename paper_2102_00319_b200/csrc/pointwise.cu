@@ -8,8 +8,12 @@ __global__ void k_add(Ctx K, heb_ct a, heb_ct b, heb_ct o, int64_t lines, int co
         const u64 p = K.pi[L.r].p;
         const u64 *x = at(a, L.b, L.c, L.r, logn), *y = at(b, L.b, L.c, L.r, logn);
         u64 *z = at(o, L.b, L.c, L.r, logn);
-        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-            z[i] = add_mod(x[i], y[i], p);
+        const ulonglong2 *x2 = reinterpret_cast<const ulonglong2 *>(x), *y2 = reinterpret_cast<const ulonglong2 *>(y);
+        ulonglong2 *z2 = reinterpret_cast<ulonglong2 *>(z);
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n / 2; i += gridDim.x * blockDim.x) {
+            const ulonglong2 u = x2[i], v = y2[i];
+            z2[i] = make_ulonglong2(add_mod(u.x, v.x, p), add_mod(u.y, v.y, p));
+        }
     }
 }
 
@@ -22,9 +26,17 @@ __global__ void k_add_plain(Ctx K, heb_ct a, const u64 *pt, int64_t pstride, heb
         const u64 *x = at(a, L.b, L.c, L.r, logn);
         u64 *z = at(o, L.b, L.c, L.r, logn);
         const u64 *y = pt + L.b * pstride + ((int64_t)L.r << logn);
-        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-            if (L.c == 0) z[i] = add_mod(x[i], y[i], p);
-            else if (copy_c1) z[i] = x[i];
+        if (L.c != 0 && !copy_c1) continue;
+        const ulonglong2 *x2 = reinterpret_cast<const ulonglong2 *>(x), *y2 = reinterpret_cast<const ulonglong2 *>(y);
+        ulonglong2 *z2 = reinterpret_cast<ulonglong2 *>(z);
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n / 2; i += gridDim.x * blockDim.x) {
+            const ulonglong2 u = x2[i];
+            if (L.c == 0) {
+                const ulonglong2 v = y2[i];
+                z2[i] = make_ulonglong2(add_mod(u.x, v.x, p), add_mod(u.y, v.y, p));
+            } else {
+                z2[i] = u;
+            }
         }
     }
 }
@@ -101,9 +113,11 @@ __global__ void k_galois(const u64 *in, u64 *out, int64_t lines, int64_t bstride
 
 extern "C" int heb_add(heb_ctx *c, heb_ct a, heb_ct b, heb_ct o, int64_t count, int comps, int k, void *stream) {
     if (!c || k < 1 || k > c->num_rows || comps < 1) return fail(HEB_EINVAL, "heb_add: bad args");
+    if ((a.ct_stride | a.comp_stride | b.ct_stride | b.comp_stride | o.ct_stride | o.comp_stride) & 1)
+        return fail(HEB_EINVAL, "heb_add: strides must be even (16-byte position pairs)");
     if (count <= 0) return HEB_OK;
     const int64_t lines = count * comps * k;
-    { PROF("k_add", (cudaStream_t)stream, 24.0 * c->n * lines); k_add<<<pw_grid(c->n, lines), 256, 0, (cudaStream_t)stream>>>(kctx(c), a, b, o, lines, comps, k, c->log_n); }
+    { PROF("k_add", (cudaStream_t)stream, 24.0 * c->n * lines); k_add<<<pw_grid(c->n / 2, lines), 256, 0, (cudaStream_t)stream>>>(kctx(c), a, b, o, lines, comps, k, c->log_n); }
     LAUNCH_CHECK();
     return HEB_OK;
 }
@@ -111,10 +125,12 @@ extern "C" int heb_add(heb_ctx *c, heb_ct a, heb_ct b, heb_ct o, int64_t count, 
 extern "C" int heb_add_plain(heb_ctx *c, heb_ct a, const uint64_t *pt, int64_t pstride, heb_ct o, int64_t count,
                              int k, void *stream) {
     if (!c || !pt || k < 1 || k > c->num_rows) return fail(HEB_EINVAL, "heb_add_plain: bad args");
+    if ((a.ct_stride | a.comp_stride | o.ct_stride | o.comp_stride | pstride) & 1)
+        return fail(HEB_EINVAL, "heb_add_plain: strides must be even (16-byte position pairs)");
     if (count <= 0) return HEB_OK;
     const int64_t lines = count * 2 * k;
     const int copy_c1 = (o.data != a.data) || (o.comp_stride != a.comp_stride) || (o.ct_stride != a.ct_stride);
-    { PROF("k_add_plain", (cudaStream_t)stream, 8.0 * c->n * (2.0 * lines + k * (pstride ? count : 1))); k_add_plain<<<pw_grid(c->n, lines), 256, 0, (cudaStream_t)stream>>>(kctx(c), a, pt, pstride, o, lines, k,
+    { PROF("k_add_plain", (cudaStream_t)stream, 8.0 * c->n * (2.0 * lines + k * (pstride ? count : 1))); k_add_plain<<<pw_grid(c->n / 2, lines), 256, 0, (cudaStream_t)stream>>>(kctx(c), a, pt, pstride, o, lines, k,
                                                                          c->log_n, copy_c1); }
     LAUNCH_CHECK();
     return HEB_OK;
