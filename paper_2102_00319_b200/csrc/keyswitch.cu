@@ -295,6 +295,38 @@ __device__ __forceinline__ void modup_store(uint32_t ta, u64 *o0, u64 *o1, int p
     }
 }
 
+// Digit staging for the FP64-engine ModUp (MODUP_STAGE): while a digit's key products
+// run (TMEM and key loads only), the next digit's row is copied into the transform's
+// shared-memory buffer with cp.async, at the padded positions the first transform group
+// reads; each thread then converts its own read set in place and the transform starts
+// from shared memory.  Hides the digit-load latency behind the products.
+#ifndef MODUP_STAGE
+#define MODUP_STAGE 1
+#endif
+template <int LL>
+__device__ __forceinline__ void stage_row_async(u64 *sm, const i64 *src) {
+    constexpr int N = 1 << LL;
+    constexpr int T = ntt::Shape<LL, 16>::T;
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sm);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < N; i += T)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(base + 8u * (uint32_t)ntt::pad(i)), "l"(src + i)
+                     : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+// the first forward group's read set of this thread (start at stage 0, shared memory)
+template <int LL, class F>
+__device__ __forceinline__ void first_group_positions(F f) {
+    using S = ntt::Shape<LL, 16>;
+    constexpr int RB0 = S::REM ? S::REM : S::LOGE;
+    constexpr int LB0 = LL - RB0;
+    constexpr int UPT0 = (S::N >> RB0) / S::T;
+#pragma unroll
+    for (int kk = 0; kk < UPT0; ++kk)
+#pragma unroll
+        for (int m = 0; m < (1 << RB0); ++m) f((int)threadIdx.x + kk * S::T + (m << LB0));
+}
+
 // TMEM columns a CTA of T threads addresses: 64 per group of four warps (one warp per
 // lane quadrant), at least 32, a power of two as tcgen05.alloc requires.  Sized to the
 // block so that as many CTAs as the NTT launch bounds make resident also fit the SM's
@@ -347,6 +379,7 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
     const int pos = tpos<LOGN>();
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         bool first = true;
+        int staged_for = -1;  // digit whose row sits in shared memory (MODUP_STAGE)
         for (int j = 0; j < k; ++j) {
             u64 y[16];
             if (j == t) {
@@ -366,8 +399,30 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
                         const ntt::FpArithRaw ar(P.pd, P.pinvd);
                         double *s2 = reinterpret_cast<double *>(sm);
                         const double *tw = K.twf + ((size_t)gt << LOGN);
-                        if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, 16>(ar, s2, tw, ld, y, rhalf<LOGN>());
-                        else ntt::forward<LL, 16>(ar, s2, tw, ld, y);
+                        if constexpr (Row<LOGN>::SPLIT) {
+                            ntt::forward_split<LL, 16>(ar, s2, tw, ld, y, rhalf<LOGN>());
+                        } else if (MODUP_STAGE && staged_for == j) {
+                            asm volatile("cp.async.wait_all;" ::: "memory");
+                            __syncthreads();
+                            first_group_positions<LL>([&](int i) {
+                                const int q = ntt::pad(i);
+                                const i64 v = reinterpret_cast<const i64 *>(sm)[q];
+                                const u64 c = ld.small ? (u64)v + (v < 0 ? ld.p : 0) : signed_mul_const(v, 1, ld.r1s, ld.p);
+                                s2[q] = ntt::u2d(c);
+                            });
+                            ntt::forward_core<LL, 16, true>(ar, s2, tw, 1, ld, y);
+                        } else {
+                            ntt::forward<LL, 16>(ar, s2, tw, ld, y);
+                        }
+                        if constexpr (MODUP_STAGE && !Row<LOGN>::SPLIT) {
+                            int jn = j + 1;
+                            if (jn == t) ++jn;
+                            if (jn < k) {
+                                __syncthreads();  // every thread has read the transform's output
+                                stage_row_async<LL>(sm, D + (b * k + jn) * n);
+                                staged_for = jn;
+                            }
+                        }
                     } else {
                         const ntt::IntArith ar(P.p);
                         const ulonglong2 *tw = K.tw + ((size_t)gt << LOGN);
