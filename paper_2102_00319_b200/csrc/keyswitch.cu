@@ -426,8 +426,32 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
                     } else {
                         const ntt::IntArith ar(P.p);
                         const ulonglong2 *tw = K.tw + ((size_t)gt << LOGN);
-                        if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, 16>(ar, sm, tw, ld, y, rhalf<LOGN>());
-                        else ntt::forward<LL, 16>(ar, sm, tw, ld, y);
+#ifndef MODUP_STAGE_INT
+#define MODUP_STAGE_INT 1
+#endif
+                        if constexpr (Row<LOGN>::SPLIT) {
+                            ntt::forward_split<LL, 16>(ar, sm, tw, ld, y, rhalf<LOGN>());
+                        } else if (MODUP_STAGE_INT && staged_for == j) {
+                            asm volatile("cp.async.wait_all;" ::: "memory");
+                            __syncthreads();
+                            first_group_positions<LL>([&](int i) {
+                                const int q = ntt::pad(i);
+                                const i64 v = reinterpret_cast<const i64 *>(sm)[q];
+                                sm[q] = ld.small ? (u64)v + (v < 0 ? ld.p : 0) : signed_mul_const(v, 1, ld.r1s, ld.p);
+                            });
+                            ntt::forward_core<LL, 16, true>(ar, sm, tw, 1, ld, y);
+                        } else {
+                            ntt::forward<LL, 16>(ar, sm, tw, ld, y);
+                        }
+                        if constexpr (MODUP_STAGE_INT && !Row<LOGN>::SPLIT) {
+                            int jn = j + 1;
+                            if (jn == t) ++jn;
+                            if (jn < k) {
+                                __syncthreads();
+                                stage_row_async<LL>(sm, D + (b * k + jn) * n);
+                                staged_for = jn;
+                            }
+                        }
                     }
                 }
             }
