@@ -1,4 +1,6 @@
-"""cfg1 mul+relin+rescale ops/s only (bench.py's secondary line), for A/B runs."""
+"""cfg1 mul+relin+rescale ops/s only (bench.py's secondary line), for A/B runs.
+
+    python tools/cfg1_bench.py [STREAMS]"""
 import json
 import os
 import sys
@@ -8,7 +10,7 @@ import bench  # noqa: E402
 
 
 class A:
-    pass
+    pipelines = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 
 
 print(json.dumps(bench.cfg1_mulrelin(A(), 0)))
