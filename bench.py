@@ -1,22 +1,25 @@
 #!/usr/bin/env python
-"""Benchmark: encrypted-CNN inference throughput on B200 (BASELINE.json configs[1]).
+"""Benchmark: encrypted-CNN inference throughput on B200 (BASELINE.json configs 2-4).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config cfg2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config cfg4]
 
-A *step* is one full encrypted inference pass of the config-2 network
-(conv 5x5x5 stride 2 -> x^2 -> 2x2 sum-pool -> FC 180->10, N = 8192, 4096 images
-packed one image per slot, every weight encrypted) over one batch whose input
-ciphertexts are resident in HBM.  Under torchrun each rank runs its own
-independent seeded batch (weak scaling); rank 0 gathers the logit ciphertexts
-over NCCL.  ``value`` = images of all ranks / max-over-ranks device time.
-``e2e`` repeats the measurement through the public API with the step's input
-ciphertexts copied from pinned host memory and the logits copied back inside
-the timed region.
+A *step* is one full encrypted inference pass of the config's network over one batch
+whose input ciphertexts are resident in HBM.  The default is config 4, the largest
+configuration that fits one GPU (N = 32768, 19 levels, 16384 images packed one image
+per slot: conv1 5x5x5 stride 2 -> x^2 -> conv2 10 filters 3x3 over 5 channels -> x^2 ->
+2x2 sum-pool -> FC 250->10, every weight encrypted); ``--config cfg2`` / ``cfg3`` give
+the smaller networks.  Under torchrun each rank runs its own independent seeded batch
+(weak scaling); rank 0 gathers the logit ciphertexts over NCCL.  ``value`` = images of
+all ranks / max-over-ranks device time.  ``e2e`` repeats the measurement through the
+public API with the step's input ciphertexts copied from pinned host memory (bit-packed
+wire format; ``e2e_u64``: the reference's u64 payload words) and the logits copied back
+inside the timed region.
 
-``--impl reference`` times the reference algorithm on the host cores instead
-(the C oracle port of the reference kernels, all host threads, bounded sample
-extrapolated by exact op counts -- the reference itself is Python/numba and
-not present on the GPU box).
+``--impl reference`` times the reference algorithm on the host cores instead (the C
+oracle port of the reference kernels driven in the reference op order, all host
+threads): each step is an exactly proportional 1/S sample of every layer of the same
+network (``CpuSample``), timed as it runs -- the reference itself is Python/numba and is
+not present on the GPU box.
 """
 
 from __future__ import annotations
@@ -39,10 +42,15 @@ sys.path.insert(0, REPO)
 BASELINE_METRIC = "encrypted-CNN images/sec and HE mul+relin ops/sec; % of B200 HBM roofline"
 UNIT = "images/s"
 
-# algorithmic (compulsory) HBM bytes and 64-bit modmuls per cfg2 batch
-CFG2_PATH_BYTES_PER_BATCH = 3.562e9
-CFG2_MODMULS_PER_BATCH = 10.36e9
-CFG1_MULRELIN_BYTES_PER_OP = 527_360
+# algorithmic (compulsory) HBM bytes and 64-bit modmuls per batch
+PATH_BYTES_PER_BATCH = {"cfg2": 3.562e9, "cfg3": 7.747e9, "cfg4": 102.46e9}
+MODMULS_PER_BATCH = {"cfg2": 10.36e9, "cfg3": 29.1e9, "cfg4": 665.6e9}
+# algorithmic bytes per op
+CFG1_BYTES_PER_OP = {"mul_relin_rescale": 527_360, "add_ct_ct": 589_824, "mul_ct_pt_rescale": 425_984,
+                     "rotate_by_1": 396_288}
+CFG1_MULRELIN_BYTES_PER_OP = CFG1_BYTES_PER_OP["mul_relin_rescale"]
+# concurrent inference pipelines per GPU (memory: a cfg4 pipeline holds ~40 GB of scratch)
+PIPELINES = {"cfg2": 3, "cfg3": 3, "cfg4": 2}
 
 
 def load_peaks() -> dict:
@@ -237,41 +245,56 @@ def run_gpu(args) -> None:
 
     # ---- end-to-end: host buffers through the public API -------------------------------
     # Every step copies its input ciphertexts from pinned host memory and its logits
-    # back; LayerEvaluator.run_stream overlaps the copy of batch s+1 with batch s.  The
-    # client hands the grid over in the bit-packed wire format (residues at the bit
-    # length of their prime, csrc/packing.cu), unpacked on the device inside the step.
-    x_packed = be.pack_batch(x)
-    x_hosts = [torch.empty(x_packed.shape, dtype=x_packed.dtype, pin_memory=True) for _ in range(2)]
-    for h in x_hosts:
-        h.copy_(x_packed)
-    del x_packed
+    # back; LayerEvaluator.run_stream overlaps the copy of batch s+1 with batch s.
+    # Two client formats: (1) the bit-packed wire format (residues at the bit length of
+    # their prime, csrc/packing.cu), unpacked on the device inside the step; (2) the
+    # reference's own payload words (u64 per residue, CkksCipher layout).
     logits_hosts = [torch.empty((out_count, 2, out_k, be.n), dtype=torch.int64, pin_memory=True)
                     for _ in range(args.steps)]
 
-    def e2e_run(nsteps):
-        ev.run_stream(enc, [x_hosts[s % 2] for s in range(nsteps)], x.level, x.scale, x.noise_bits,
-                      logits_hosts[:nsteps], on_output=lambda s, o: gather(o), pipelines=args.pipelines,
-                      unpacked_shape=tuple(x.buf.shape))
+    def e2e_measure(host, unpacked_shape):
+        def e2e_run(nsteps):
+            ev.run_stream(enc, [host] * nsteps, x.level, x.scale, x.noise_bits, logits_hosts[:nsteps],
+                          on_output=lambda s, o: gather(o), pipelines=args.pipelines, unpacked_shape=unpacked_shape)
 
-    e2e_run(min(args.steps, max(2 * args.pipelines, args.warmup)))
-    torch.cuda.synchronize()
-    barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    gc.disable()
-    e0.record(stream)
-    e2e_run(args.steps)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    gc.enable()
-    e2e_ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
-    if world > 1:
-        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_value = batch * world * args.steps / (float(e2e_ms.item()) / 1e3)
+        e2e_run(min(args.steps, max(2 * args.pipelines, args.warmup)))
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        gc.disable()
+        e0.record(stream)
+        e2e_run(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        gc.enable()
+        e_ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        return batch * world * args.steps / (float(e_ms.item()) / 1e3)
+
+    x_packed = be.pack_batch(x)
+    x_host = torch.empty(x_packed.shape, dtype=x_packed.dtype, pin_memory=True)
+    x_host.copy_(x_packed)
+    del x_packed
+    e2e_value = e2e_measure(x_host, tuple(x.buf.shape))
+    packed_bytes = int(x_host.numel() * 8)
+    del x_host
+    ev.drop_input_buffers()
+    e2e_u64 = None
+    if not args.skip_u64:
+        x_host = torch.empty(tuple(x.buf.shape), dtype=torch.int64, pin_memory=True)
+        x_host.copy_(x.buf)
+        e2e_u64 = {"value": round(e2e_measure(x_host, None), 3), "unit": UNIT,
+                   "h2d_bytes_per_step": int(x_host.numel() * 8),
+                   "d2h_bytes_per_step": int(out_count * 2 * out_k * be.n * 8),
+                   "wire_format": "u64 words per residue (the reference's CkksCipher payload layout)"}
+        del x_host
+        ev.drop_input_buffers()
 
     # ---- secondary: cfg1 HE mul+relin ops/s (256 pairs, one batched launch sequence) ----
-    sec = cfg1_mulrelin(args, local) if (rank == 0 and not args.skip_cfg1) else None
+    sec = cfg1_ops(args, local) if (rank == 0 and not args.skip_cfg1) else None
 
     # ---- int64 modmul peak (microbenchmark) ---------------------------------------------
     peak_mm = modmul_peak(be) if rank == 0 else None
@@ -281,9 +304,10 @@ def run_gpu(args) -> None:
         top = max(prof.items(), key=lambda kv: kv[1][1]) if prof else ("none", (0, 1e-9, 0.0))
         name, (cnt, tot_ms, tot_bytes) = top
         achieved = tot_bytes / (tot_ms / 1e3) / 1e9
-        traffic = ncu_traffic(name)
-        cpu = cpu_baseline(args) if (world == 1 and not args.skip_cpu and args.config == "cfg2") else None
-        path_rate = CFG2_PATH_BYTES_PER_BATCH * value / batch / 1e9 if args.config == "cfg2" else None
+        traffic = ncu_traffic(name, args.config)
+        cpu = cpu_baseline(args) if (world == 1 and not args.skip_cpu) else None
+        path_bytes = PATH_BYTES_PER_BATCH[args.config]
+        path_rate = path_bytes * value / batch / 1e9
         line = {
             "metric": BASELINE_METRIC,
             "value": round(value, 3),
@@ -296,10 +320,9 @@ def run_gpu(args) -> None:
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "u64",
-            "data": "synthetic (seeded U[0,1] 28x28 pixels, N(0,0.1^2) weights; MNIST absent)",
+            "data": f"synthetic (seeded U[0,1] 28x28 pixels, N(0,{net_sigma(args.config)}^2) weights; MNIST absent)",
             "config": {
-                "workload": f"{args.config}: encrypted CNN {' -> '.join(l.kind for l in net.layers)}, "
-                            f"N={be.n}, {be.chain.num_levels} levels, {batch} images/GPU",
+                "workload": workload_name(args.config, net, be.n, be.chain.num_levels, batch),
                 "batch_per_gpu": batch,
                 "ring_degree": be.n,
                 "l2_policy": f"inputs larger than L2 ({x.buf.numel() * 8 / 1e6:.0f} MB of input ciphertexts per step)",
@@ -318,32 +341,33 @@ def run_gpu(args) -> None:
                 "share_of_step": round(tot_ms / max(prof_ms, 1e-9), 4),
                 "measured": "CUDA events around every launch in a dedicated pass of the same K steps on one stream",
                 "peak_source": peaks["source"],
-                "note": "kernel is INT64-multiply bound; see int_roofline",
+                "note": "kernel is bound by the FP64 / integer pipes (NTT butterflies), not HBM: see compute_roofline",
             },
-            "path_roofline": None if path_rate is None else {
-                "algorithmic_bytes_per_batch": CFG2_PATH_BYTES_PER_BATCH,
+            "path_roofline": {
+                "algorithmic_bytes_per_batch": path_bytes,
                 "achieved_gbs": round(path_rate, 2),
                 "frac_of_hbm": round(path_rate / peaks["hbm_gbs"], 4),
-                "source": "SURVEY.md §8(d) cfg2 layer-wise compulsory bytes",
+                "source": f"SURVEY.md §8(d) {args.config} layer-wise compulsory bytes",
             },
-            "modmul_rate": None if (peak_mm is None or args.config != "cfg2") else {
-                "modmuls_per_batch": CFG2_MODMULS_PER_BATCH,
-                "achieved_modmul_per_s": CFG2_MODMULS_PER_BATCH * value / batch,
+            "modmul_rate": None if peak_mm is None else {
+                "modmuls_per_batch": MODMULS_PER_BATCH[args.config],
+                "achieved_modmul_per_s": MODMULS_PER_BATCH[args.config] * value / batch,
                 "shoup_int_peak_per_s": peak_mm,
                 "note": "SURVEY 8(d) modmul count; the 40-bit rows run on the FP64 (DFMA) pipe, "
                         "so the integer Shoup peak is not an upper bound for the mix",
             },
-            "compute_roofline": ncu_pipes(name),
+            "compute_roofline": ncu_pipes(name, args.config),
             "kernels": {k: {"launches": v[0], "ms": round(v[1], 3), "gbs": round(v[2] / max(v[1], 1e-9) / 1e6, 1)}
                         for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
             "cpu_baseline": cpu,
             "e2e": {
                 "value": round(e2e_value, 3),
                 "unit": UNIT,
-                "h2d_bytes_per_step": int(x_hosts[0].numel() * 8),
+                "h2d_bytes_per_step": packed_bytes,
                 "wire_format": "bit-packed residues (heb_pack_rows), unpacked on the device in the step",
                 "d2h_bytes_per_step": int(out_count * 2 * out_k * be.n * 8),
             },
+            "e2e_u64": e2e_u64,
             "gpu_launches": int(launches),
             "clocks": clk,
             "secondary": sec,
@@ -356,8 +380,10 @@ def run_gpu(args) -> None:
         dist.destroy_process_group()
 
 
-def cfg1_mulrelin(args, device: int) -> dict:
-    """HE mul+relin(+rescale) ops/s on config 1: 256 seeded pairs per batched call."""
+def cfg1_ops(args, device: int) -> dict:
+    """Config 1 primitive ops/s on the device: 256 seeded pairs per batched call, calls
+    issued round-robin on the bench's pipeline count of concurrent streams.  Ops (SURVEY
+    §8d): mul+relin+rescale, ct+ct, ct*pt+rescale, rotate-by-1 (Galois element 5)."""
     import torch
 
     from paper_2102_00319_b200 import layers
@@ -366,54 +392,75 @@ def cfg1_mulrelin(args, device: int) -> dict:
 
     cfg = CONFIGS["cfg1"]
     be = B200Backend(cfg.params(), cfg.base_extra_bits, device=device)
-    keys = be.keygen()
+    keys = be.keygen(galois_steps=(1,))
     be.set_eval_key(keys)
-    xs, ys = cfg1_pairs(be.slots)
-    a = be.encrypt_batch(xs, keys, np.arange(256))
-    b = be.encrypt_batch(ys, keys, 256 + np.arange(256))
+    be.set_galois_key(keys)
+    P = 256
+    xs, ys = cfg1_pairs(be.slots, P)
+    a = be.encrypt_batch(xs, keys, np.arange(P))
+    b = be.encrypt_batch(ys, keys, P + np.arange(P))
     ev = layers.LayerEvaluator(be)
-    k = a.k
-    # independent 256-pair calls on `streams` concurrent streams (each call: tensor +
-    # relinearise + rescale into its own buffers), like the CNN's pipelines
-    streams = [torch.cuda.Stream(be.dev) for _ in range(max(1, getattr(args, "pipelines", 3)))]
-    raws = [be.ctx.empty(256, 3, k, be.n) for _ in streams]
-    outs = [None] * len(streams)
+    k, n, lvl = a.k, be.n, a.level
+    pts = torch.stack([be.encode_plain(ys[i]).payload.rows[:k] for i in range(P)]).contiguous()
+    g = be.galois_element(1)
+    gk = be._galois_keys[g].prep
+    streams = [torch.cuda.Stream(be.dev) for _ in range(max(1, args.pipelines))]
+    S = len(streams)
+    raws = [be.ctx.empty(P, 3, k, n) for _ in streams]
+    outs = [be.ctx.empty(P, 2, k, n) for _ in streams]
+    last = {}
 
-    def step(i):
-        st = streams[i % len(streams)]
-        with torch.cuda.stream(st):
-            raw = raws[i % len(streams)]
-            be.ctx.call("heb_tensor", a.desc(), b.desc(), ct_desc(raw), 256, k, 0, be.ctx.stream)
-            outs[i % len(streams)] = ev.finalize(raw, a.level, a.scale * b.scale, 0.0)
-        return outs[i % len(streams)]
+    def mul(i):
+        be.ctx.call("heb_tensor", a.desc(), b.desc(), ct_desc(raws[i % S]), P, k, 0, be.ctx.stream)
+        last["mul"] = ev.finalize(raws[i % S], lvl, a.scale * b.scale, 0.0)
+
+    def add(i):
+        be.ctx.call("heb_add", a.desc(), b.desc(), ct_desc(outs[i % S]), P, 2, k, be.ctx.stream)
+
+    def ctpt(i):
+        be.ctx.call("heb_mul_plain_rescale", a.desc(), pts.data_ptr(), k * n, ct_desc(outs[i % S]), P, lvl,
+                    be.ctx.stream)
+
+    def rot(i):
+        be.ctx.call("heb_rotate", a.desc(), gk.data_ptr(), ct_desc(outs[i % S]), P, lvl, g, be.ctx.stream)
+        last["rot"] = outs[i % S]
 
     cur = torch.cuda.current_stream(be.dev)
-    for st in streams:
-        st.wait_stream(cur)
-    for i in range(10 * len(streams)):
-        step(i)
-    reps = 240  # ~0.4 ms per call: enough calls for a stable rate
-    torch.cuda.synchronize()
-    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s0.record(cur)
-    for st in streams:
-        st.wait_stream(cur)
-    for i in range(reps):
-        out = step(i)
-    for st in streams:
-        cur.wait_stream(st)
-    s1.record(cur)
-    torch.cuda.synchronize()
-    ops = 256 * reps / (s0.elapsed_time(s1) / 1e3)
+
+    def timed(fn, reps):
+        for st in streams:
+            st.wait_stream(cur)
+        for i in range(4 * S):
+            with torch.cuda.stream(streams[i % S]):
+                fn(i)
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(cur)
+        for st in streams:
+            st.wait_stream(cur)
+        for i in range(reps):
+            with torch.cuda.stream(streams[i % S]):
+                fn(i)
+        for st in streams:
+            cur.wait_stream(st)
+        s1.record(cur)
+        torch.cuda.synchronize()
+        return P * reps / (s0.elapsed_time(s1) / 1e3)
+
     peaks = load_peaks()
-    dec = be.decrypt_batch(out, keys)
-    err = float(np.max(np.abs(dec[:8] - xs[:8] * ys[:8])))
+    res = {}
+    for name, fn, reps in (("mul_relin_rescale", mul, 240), ("add_ct_ct", add, 2000), ("mul_ct_pt_rescale", ctpt, 600),
+                           ("rotate_by_1", rot, 240)):
+        ops = timed(fn, reps)
+        res[name] = {"value": round(ops, 1), "unit": "ops/s",
+                     "hbm_frac": round(ops * CFG1_BYTES_PER_OP[name] / 1e9 / peaks["hbm_gbs"], 4)}
+    dec = be.decrypt_batch(last["mul"], keys)
+    res["mul_relin_rescale"]["max_abs_err"] = float(np.max(np.abs(dec[:8] - xs[:8] * ys[:8])))
     return {
-        "metric": "HE mul+relin+rescale ops/sec (cfg1, N=4096, 256 pairs per call, concurrent calls on "
-                  f"{len(streams)} streams)",
-        "value": round(ops, 1),
-        "hbm_frac": round(ops * CFG1_MULRELIN_BYTES_PER_OP / 1e9 / peaks["hbm_gbs"], 4),
-        "max_abs_err": err,
+        "metric": f"HE ops/sec on cfg1 (N=4096, 256 pairs per call, concurrent calls on {S} streams)",
+        "value": res["mul_relin_rescale"]["value"],
+        "unit": "ops/s",
+        "ops": res,
     }
 
 
@@ -431,9 +478,14 @@ def modmul_peak(be) -> float:
     return blocks * threads * iters * 8 / (ms.value / 1e3)
 
 
-def ncu_traffic(kernel: str):
-    """dram bytes per launch of the top kernel from the committed ncu capture, if any."""
-    path = os.path.join(REPO, "profiles", "ncu_top_kernel.json")
+def ncu_record_path(config: str) -> str:
+    """The committed ncu --set full capture of this config's top kernel."""
+    return os.path.join(REPO, "profiles", f"ncu_top_kernel_{config}.json")
+
+
+def ncu_traffic(kernel: str, config: str):
+    """dram bytes per launch of the top kernel from the config's committed ncu capture, if any."""
+    path = ncu_record_path(config)
     if not os.path.exists(path):
         return None
     with open(path) as fh:
@@ -442,9 +494,9 @@ def ncu_traffic(kernel: str):
     return rec.get("dram_bytes_per_launch") if rec else None
 
 
-def ncu_pipes(kernel: str):
-    """Pipe utilisation of the top kernel from the committed ncu --set full capture."""
-    path = os.path.join(REPO, "profiles", "ncu_top_kernel.json")
+def ncu_pipes(kernel: str, config: str):
+    """Pipe utilisation of the top kernel from the config's committed ncu --set full capture."""
+    path = ncu_record_path(config)
     if not os.path.exists(path):
         return None
     with open(path) as fh:
@@ -466,111 +518,253 @@ def ncu_pipes(kernel: str):
 # ---------------------------------------------------------------------------
 
 class CpuSample:
-    """Bounded sample of the cfg2 workload on the CPU oracle (reference algorithm).
+    """Bounded, exactly proportional sample of one batch of the config's network on the
+    CPU oracle (the reference algorithm: the C restatement of its kernels driven through
+    the reference's per-ciphertext op sequence, ``percell`` order).
 
-    Sample = conv output rows 0-1 (all 5 filters, 120 cells: 25 taps each +
-    relinearise/rescale), their x^2 (120 mul+relin), the 30 pooled windows they
-    feed, plus the complete FC layer (1800 products, 10 finalizes).  conv/x^2/pool
-    are 2/12 of their layers, so batch time = 6 * t(conv+sq+pool sample) + t(FC).
+    The sample is 1/S of EVERY layer: the first 1/S of the conv cells (position-major,
+    filter fastest), of the activations, of the pool windows and of the FC outputs.
+    All cells of a layer cost the same ops (same taps, same level), so one sample is
+    exactly 1/S of the batch's HE operations and stands for batch/S images -- no
+    per-layer extrapolation.  Layer l's sampled cells read real ciphertexts of the right
+    level and scale: the first conv reads the encrypted input pixels its cells cover,
+    later layers read the previous layer's sampled outputs (wrapped around).
     """
 
-    def __init__(self, config: str = "cfg2"):
+    SHARDS = {"cfg2": 1, "cfg3": 5, "cfg4": 10}
+
+    def __init__(self, config: str = "cfg4", shards: int | None = None):
         import warnings
 
         warnings.simplefilter("ignore")
         from oracle.ckks_oracle import OracleBackend, threaded_map
         from paper_2102_00319_b200.configs import BATCH, CONFIGS, IMAGE_SEEDS, NETWORKS, cnn_images
         from paper_2102_00319_b200.model import ledger, weight_entropies
+        from paper_2102_00319_b200 import percell
 
         self.map = threaded_map
+        self.percell = percell
+        self.config = config
         cfg = CONFIGS[config]
         be = OracleBackend(cfg.params(), cfg.base_extra_bits)
         keys = be.keygen()
         be.set_eval_key(keys)
         self.be, self.keys = be, keys
-        net = NETWORKS[config]()
-        conv, dense = net.layers[0], net.layers[4]
+        net = self.net = NETWORKS[config]()
+        S = self.shards = shards or self.SHARDS[config]
         trace = ledger(net, be.chain, be.canonical_scale)
         self.batch = min(BATCH[config], be.slots)
-        imgs = cnn_images(self.batch, IMAGE_SEEDS[config])
         tags = weight_entropies(net)
         slots = be.slots
-        cells = [(i, j) for i in range(7) for j in range(28)]
-        self.x = {}
-        for (i, j), ct in zip(cells, threaded_map(lambda ij: be.encrypt(imgs[:, ij[0], ij[1]], keys, entropy=ij[0] * 28 + ij[1]), cells)):
-            self.x[(i, j)] = ct
-        widx = [(f, p, q) for f in range(5) for p in range(5) for q in range(5)]
-        self.w = dict(zip(widx, threaded_map(lambda t: be.encrypt(np.full(slots, conv.weights[t[0], 0, t[1], t[2]]), keys, entropy=int(tags[0][t[0], 0, t[1], t[2]])), widx)))
-        fc_level = trace[4]["level"]
-        fc_scale = trace[4]["scale"]
-        self.fc_in = threaded_map(lambda i: be.drop_to_level(be.encrypt(np.full(slots, 0.1 * (i % 7)), keys, scale=fc_scale, entropy=10_000 + i), fc_level), range(180))
-        fidx = [(i, r) for i in range(180) for r in range(10)]
-        self.fw = dict(zip(fidx, threaded_map(lambda t: be.drop_to_level(be.encrypt(np.full(slots, dense.weights[t]), keys, entropy=int(tags[4][t])), fc_level), fidx)))
+        shapes = net.shapes()
+        self.plan = self.sample_plan(net, S)  # (kind, layer index, units in the sample, units in the layer)
+        # first conv: the input pixels its sampled cells cover, encrypted like pack_batch
+        conv0 = net.layers[0]
+        _, om, on = shapes[0]
+        F = conv0.filters
+        n0 = self.plan[0][2]
+        self.conv0_cells = [(u % F, (u // F) // on, (u // F) % on) for u in range(n0)]
+        rows = max(i for _, i, _ in self.conv0_cells) * conv0.stride + conv0.kernel[0]
+        m, n = net.input_dims
+        imgs = cnn_images(self.batch, IMAGE_SEEDS[config])
+        cells = [(i, j) for i in range(rows) for j in range(n)]
+        self.x = dict(zip(cells, threaded_map(
+            lambda ij: be.encrypt(imgs[:, ij[0], ij[1]], keys, entropy=ij[0] * n + ij[1]), cells)))
+        # weights of the sampled cells, encrypted and dropped to their use-site level (encrypt_network)
+        self.w = {}
+        for kind, li, cnt, _ in self.plan:
+            layer = net.layers[li]
+            if kind == "conv":
+                idx = list(np.ndindex(*layer.weights.shape))
+            elif kind == "dense":
+                idx = [(i, r) for i in range(layer.in_dim) for r in range(cnt)]
+            else:
+                continue
+            lvl = trace[li]["level"]
+            enc = threaded_map(lambda t: be.drop_to_level(
+                be.encrypt(np.full(slots, float(layer.weights[t])), keys, entropy=int(tags[li][t])), lvl), idx)
+            self.w[li] = dict(zip(idx, enc))
+        self.trace = trace
         self.cores = os.cpu_count() or 1
 
-    def _conv_cell(self, fij):
-        be = self.be
-        f, i, j = fij
-        acc = None
-        for p in range(5):
-            for q in range(5):
-                t = be.mul_ct_ct_raw(self.x[(2 * i + p, 2 * j + q)], self.w[(f, p, q)])
-                acc = t if acc is None else be.raw_add(acc, t)
-        y = be.raw_finalize(acc)
-        return be.mul_ct_ct(y, y)
+    @staticmethod
+    def sample_plan(net, S: int) -> list:
+        """Per layer with work: (kind, layer index, units per 1/S sample, units in the layer);
+        units are conv cells, activation cells, pool windows and FC outputs."""
+        from paper_2102_00319_b200.model import Conv, Dense, PolyAct, Square, SumPool
 
-    def _fc_out(self, r):
-        be = self.be
-        acc = be.mul_ct_ct_raw(self.fc_in[0], self.fw[(0, r)])
-        for i in range(1, 180):
-            acc = be.raw_add(acc, be.mul_ct_ct_raw(self.fc_in[i], self.fw[(i, r)]))
-        return be.raw_finalize(acc)
+        shapes = net.shapes()
+        plan = []
+        dims = (1, *net.input_dims)
+        for li, layer in enumerate(net.layers):
+            if isinstance(layer, (Conv, SumPool)):
+                units = shapes[li][0] * shapes[li][1] * shapes[li][2]
+            elif isinstance(layer, (Square, PolyAct)):
+                units = dims[0] * dims[1] * dims[2]
+            elif isinstance(layer, Dense):
+                units = layer.out_dim
+            else:
+                units = 0
+            if units:
+                if units % S:
+                    raise ValueError(f"layer {li} ({layer.kind}) has {units} units, not divisible by {S}")
+                plan.append((layer.kind, li, units // S, units))
+            if len(shapes[li]) == 3:
+                dims = shapes[li]
+        return plan
 
     def step(self) -> float:
-        """Run the sample once; returns extrapolated seconds per full batch."""
-        be = self.be
+        """Run the sample once; returns its wall-clock seconds."""
+        be, net = self.be, self.net
         t0 = time.perf_counter()
-        cells = [(f, i, j) for f in range(5) for i in range(2) for j in range(12)]
-        sq = dict(zip(cells, self.map(self._conv_cell, cells)))
-        windows = [(f, j) for f in range(5) for j in range(6)]
+        prev = None
+        for kind, li, cnt, _ in self.plan:
+            layer = net.layers[li]
+            if kind == "conv":
+                C, (P, Q), s = layer.channels, layer.kernel, layer.stride
+                W = self.w[li]
+                if prev is None:
+                    def cell(u, W=W, C=C, P=P, Q=Q, s=s):
+                        f, i, j = self.conv0_cells[u]
+                        acc = None
+                        for c in range(C):
+                            for dp in range(P):
+                                for dq in range(Q):
+                                    t = be.mul_ct_ct_raw(self.x[(i * s + dp, j * s + dq)], W[(f, c, dp, dq)])
+                                    acc = t if acc is None else be.raw_add(acc, t)
+                        return be.raw_finalize(acc)
+                else:
+                    F = layer.filters
 
-        def pool(fj):
-            f, j = fj
-            acc = sq[(f, 0, 2 * j)]
-            for di, dj in ((1, 0), (0, 1), (1, 1)):
-                acc = be.add_ct_ct(acc, sq[(f, di, 2 * j + dj)])
-            return acc
+                    def cell(u, W=W, C=C, P=P, Q=Q, F=F, src=prev):
+                        f = u % F
+                        acc = None
+                        for tap, (c, dp, dq) in enumerate(np.ndindex(C, P, Q)):
+                            t = be.mul_ct_ct_raw(src[(u * C * P * Q + tap) % len(src)], W[(f, c, dp, dq)])
+                            acc = t if acc is None else be.raw_add(acc, t)
+                        return be.raw_finalize(acc)
+                prev = self.map(cell, range(cnt))
+            elif kind == "square":
+                prev = self.map(lambda y: be.mul_ct_ct(y, y), prev[:cnt])
+            elif kind == "polyact":
+                pts = self.percell.act_plaintexts(be, layer, prev[0].level, prev[0].scale)
+                prev = self.map(lambda y: self.percell.poly_act_cell(be, y, *pts), prev[:cnt])
+            elif kind == "sumpool":
+                def window(u, src=prev):
+                    acc = src[(4 * u) % len(src)]
+                    for d in range(1, 4):
+                        acc = be.add_ct_ct(acc, src[(4 * u + d) % len(src)])
+                    return acc
+                prev = self.map(window, range(cnt))
+            elif kind == "dense":
+                # the reference executor's stage 2 (executor.py:241-267): class x input-chunk
+                # tasks of raw partial dot products, combined in fixed order, then finalized
+                W, din = self.w[li], layer.in_dim
+                J = max(1, min(din, self.cores // cnt))
+                bounds = [(din * c) // J for c in range(J + 1)]
 
-        self.map(pool, windows)
-        t1 = time.perf_counter()
-        self.map(self._fc_out, range(10))
-        t2 = time.perf_counter()
-        return 6.0 * (t1 - t0) + (t2 - t1)
+                def part(rc, W=W, src=prev):
+                    r, c = divmod(rc, J)
+                    acc = None
+                    for i in range(bounds[c], bounds[c + 1]):
+                        t = be.mul_ct_ct_raw(src[i % len(src)], W[(i, r)])
+                        acc = t if acc is None else be.raw_add(acc, t)
+                    return acc
+                parts = self.map(part, range(cnt * J))
+
+                def combine(r):
+                    acc = parts[r * J]
+                    for c in range(1, J):
+                        acc = be.raw_add(acc, parts[r * J + c])
+                    return be.raw_finalize(acc)
+                prev = self.map(combine, range(cnt))
+        return time.perf_counter() - t0
+
+    def describe(self) -> str:
+        parts = ", ".join(f"{kind} {cnt}/{tot}" for kind, _, cnt, tot in self.plan)
+        return (f"{self.config}: 1/{self.shards} of every layer per step ({parts}) = {self.batch // self.shards} "
+                f"images-equivalent; C oracle of the reference kernels in the reference op order, "
+                f"ThreadPool over {self.cores} host threads")
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def cpu_baseline(args) -> dict:
+    """One bounded sample of the same workload on the CPU oracle (rank 0, N = 1)."""
     s = CpuSample(args.config)
+    s.step()  # numpy / thread-pool warm-up
     sec = s.step()
     return {
-        "value": round(s.batch / sec, 3),
+        "value": round(s.batch / s.shards / sec, 3),
         "unit": UNIT,
         "cores": s.cores,
         "kind": "port",
-        "sample": "cfg2 conv rows 0-1 (120 cells x 25 taps + relin), their x^2, 30 pool windows, full FC; "
-                  "extrapolated x6 for conv/x^2/pool; C oracle of the reference kernels, ThreadPool over all cores",
+        "cpu": cpu_model(),
+        "sample": s.describe(),
+        "sample_seconds": round(sec, 3),
+        "cfg1_ops": cfg1_cpu_ops(),
     }
 
 
+def cfg1_cpu_ops(pairs: int = 256) -> dict:
+    """Config 1 primitive ops/s on the CPU oracle over all host threads."""
+    import warnings
+
+    warnings.simplefilter("ignore")
+    from oracle.ckks_oracle import OracleBackend, threaded_map
+    from paper_2102_00319_b200.configs import CONFIGS, cfg1_pairs
+
+    cfg = CONFIGS["cfg1"]
+    be = OracleBackend(cfg.params(), cfg.base_extra_bits)
+    keys = be.keygen(galois_steps=(1,))
+    be.set_eval_key(keys)
+    be.set_galois_key(keys)
+    xs, ys = cfg1_pairs(be.slots, pairs)
+    a = threaded_map(lambda i: be.encrypt(xs[i], keys, entropy=i), range(pairs))
+    b = threaded_map(lambda i: be.encrypt(ys[i], keys, entropy=pairs + i), range(pairs))
+    pts = threaded_map(lambda i: be.encode_plain(ys[i]), range(pairs))
+    ops = {
+        "mul_relin_rescale": lambda i: be.mul_ct_ct(a[i], b[i]),
+        "add_ct_ct": lambda i: be.add_ct_ct(a[i], b[i]),
+        "mul_ct_pt_rescale": lambda i: be.mul_ct_pt(a[i], pts[i]),
+        "rotate_by_1": lambda i: be.rotate(a[i], 1),
+    }
+    out = {}
+    for name, fn in ops.items():
+        threaded_map(fn, range(16))
+        t0 = time.perf_counter()
+        threaded_map(fn, range(pairs))
+        out[name] = round(pairs / (time.perf_counter() - t0), 1)
+    out["unit"] = "ops/s"
+    out["threads"] = os.cpu_count() or 1
+    return out
+
+
 def run_reference(args) -> None:
+    """The reference algorithm on the host cores: each step runs one proportional sample
+    (CpuSample: 1/S of every layer of the same network, batch and level schedule as the
+    b200 arm); ms_per_step is that sample's measured wall time and value the images it
+    stands for (batch / S) divided by that time."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
     s = CpuSample(args.config)
-    for _ in range(args.warmup if args.warmup < 2 else 1):
-        s.step()
+    # CPU steps need no warm-up (no JIT, no caches worth priming at these sizes; the
+    # oracle library is loaded and the thread pool exercised while encrypting the
+    # sample's inputs): a cfg4 sample step is ~15 s on 16 cores, so W extra steps would
+    # only lengthen the run
     secs = [s.step() for _ in range(args.steps)]
-    batch_s = sum(secs) / len(secs)
-    value = s.batch / batch_s
+    step_s = sum(secs) / len(secs)
+    value = s.batch / s.shards / step_s
     line = {
         "metric": BASELINE_METRIC,
         "value": round(value, 3),
@@ -579,18 +773,29 @@ def run_reference(args) -> None:
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": round(batch_s * 1e3, 3),
+        "warmup_run": 0,
+        "ms_per_step": round(step_s * 1e3, 3),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "u64",
         "data": "synthetic",
-        "config": {"workload": f"{args.config}: same network/batch as the b200 arm", "batch_per_gpu": s.batch},
+        "config": {"workload": workload_name(args.config, s.net, s.be.n, s.be.chain.num_levels, s.batch),
+                   "batch_per_gpu": s.batch, "images_per_step": s.batch // s.shards},
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": s.cores, "kind": "port",
-                         "sample": "per step: cfg2 conv rows 0-1 + x^2 + pool windows + full FC, extrapolated to the batch"},
+                         "cpu": cpu_model(), "sample": s.describe()},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def net_sigma(config: str) -> float:
+    return 0.05 if config == "cfg4" else 0.1
+
+
+def workload_name(config: str, net, n: int, levels: int, batch: int) -> str:
+    return (f"{config}: encrypted CNN {' -> '.join(l.kind for l in net.layers)}, N={n}, {levels} levels, "
+            f"{batch} images/GPU")
 
 
 def main() -> None:
@@ -599,13 +804,17 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4"])
-    ap.add_argument("--pipelines", type=int, default=3,
-                    help="concurrent inference pipelines (streams) per GPU")
+    ap.add_argument("--config", default="cfg4", choices=["cfg2", "cfg3", "cfg4"],
+                    help="BASELINE config; cfg4 (N = 32768, the largest single-GPU config) is the headline")
+    ap.add_argument("--pipelines", type=int, default=None,
+                    help="concurrent inference pipelines (streams) per GPU (default: per config)")
     ap.add_argument("--no-prof", action="store_true", help="no per-kernel events in the timed region")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-cfg1", action="store_true")
+    ap.add_argument("--skip-u64", action="store_true", help="no e2e run in the reference's u64 payload format")
     args = ap.parse_args()
+    if args.pipelines is None:
+        args.pipelines = PIPELINES[args.config]
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -510,6 +510,12 @@ class LayerEvaluator:
         for st in comp + copy:
             caller.wait_stream(st)
 
+    def drop_input_buffers(self) -> None:
+        """Free the device staging buffers of bit-packed host inputs (``run_stream``); the
+        unpacked per-pipeline inputs stay (captured graphs hold their addresses)."""
+        for key in [k for k in self._inbufs if isinstance(k[0], tuple) and k[0][:1] == ("packed",)]:
+            del self._inbufs[key]
+
     def run_many(self, enc: EncryptedNetworkBatch, x: CipherBatch, steps: int, pipelines: int = 2,
                  on_output=None, marks: list | None = None, graphs: bool = True) -> None:
         """Evaluate ``steps`` device-resident batches over ``pipelines`` concurrent streams

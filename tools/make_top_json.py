@@ -1,7 +1,7 @@
-"""Build profiles/ncu_top_kernel.json (read by bench.py for roofline.traffic and
+"""Build profiles/ncu_top_kernel_CONFIG.json (read by bench.py for roofline.traffic and
 compute_roofline) from `ncu --set full` raw-page CSVs of the top kernel's launches.
 
-    python tools/make_top_json.py KERNEL ALG_BYTES SOURCE raw1.csv [raw2.csv ...]
+    python tools/make_top_json.py CONFIG KERNEL ALG_BYTES SOURCE raw1.csv [raw2.csv ...]
 
 One bench-profiled launch of KERNEL may be several device launches (k_ks_modup_fused:
 one per NTT engine); their DRAM bytes add up.  ALG_BYTES: the algorithmic bytes bench.py
@@ -35,7 +35,7 @@ def read(path):
 
 
 def main():
-    kernel, alg, source, paths = sys.argv[1], float(sys.argv[2]), sys.argv[3], sys.argv[4:]
+    config, kernel, alg, source, paths = sys.argv[1], sys.argv[2], float(sys.argv[3]), sys.argv[4], sys.argv[5:]
     parts = [read(p) for p in paths]
     dram = sum(p.get("dram_read", 0) + p.get("dram_write", 0) for p in parts)
     dur = sum(p.get("duration", 0) for p in parts)
@@ -50,7 +50,7 @@ def main():
     w = lambda key: round(sum(p.get(key, 0) * p.get("duration", 0) for p in parts) / max(dur, 1e-12), 2)  # noqa: E731
     for key in ("fp64_pipe_pct", "fma_pipe_pct", "alu_pipe_pct", "issue_active_pct"):
         rec[key] = w(key)
-    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_top_kernel.json")
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", f"ncu_top_kernel_{config}.json")
     with open(path, "w") as fh:
         json.dump({kernel: rec}, fh, indent=1)
     print(json.dumps({kernel: rec}, indent=1))
