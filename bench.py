@@ -49,8 +49,8 @@ MODMULS_PER_BATCH = {"cfg2": 10.36e9, "cfg3": 29.1e9, "cfg4": 665.6e9}
 CFG1_BYTES_PER_OP = {"mul_relin_rescale": 527_360, "add_ct_ct": 589_824, "mul_ct_pt_rescale": 425_984,
                      "rotate_by_1": 396_288}
 CFG1_MULRELIN_BYTES_PER_OP = CFG1_BYTES_PER_OP["mul_relin_rescale"]
-# concurrent inference pipelines per GPU (memory: a cfg4 pipeline holds ~40 GB of scratch)
-PIPELINES = {"cfg2": 3, "cfg3": 3, "cfg4": 2}
+# concurrent inference pipelines per GPU (a second cfg4 pipeline runs out of HBM)
+PIPELINES = {"cfg2": 3, "cfg3": 3, "cfg4": 1}
 
 
 def load_peaks() -> dict:

@@ -169,33 +169,38 @@ static inline Ctx kctx(const heb_ctx *c) {
 }
 
 // ---------------------------------------------------------------------------------
-// Row geometry.  Rows of N <= 2^14 residues are owned by one CTA; N = 2^15 rows are
-// split over a 2-CTA cluster (blockIdx.x = 2 * logical index + half).  Kernels use
-// lbx() for their logical x index, tpos() for the first of the positions a thread
-// holds after a forward transform (line pairs: tpos + (m & 1) + 2 T (m >> 1), see
-// ntt::lpos; load16/store16 walk that pattern), KT for their block size.
+// Row geometry.  A CTA owns 2^LL residues of a row, LL = min(log N, ROW_MAX_LL); longer
+// rows are split over an SP-CTA cluster (SP = N / 2^LL = 2 or 4, blockIdx.x = SP *
+// logical index + part): parts of 2^13 residues (68 KB of shared memory, 512 threads)
+// let two CTAs share an SM, where a 2^14 part (136 KB) leaves one barrier-synchronised
+// CTA per SM.  Kernels use lbx() for their logical x index, rpart() for their part,
+// tpos() for the first of the positions a thread holds after a forward transform (line
+// pairs: tpos + (m & 1) + 2 T (m >> 1), see ntt::lpos; load16/store16 walk that
+// pattern), KT for their block size.
+#ifndef ROW_MAX_LL
+#define ROW_MAX_LL 14
+#endif
 template <int LOGN>
 struct Row {
-#ifndef SPLIT_MIN_LOGN
-#define SPLIT_MIN_LOGN 15
-#endif
-    static constexpr bool SPLIT = LOGN >= SPLIT_MIN_LOGN;
-    static constexpr int LL = SPLIT ? LOGN - 1 : LOGN;  // residues per CTA = 2^LL
+    static constexpr int LL = LOGN < ROW_MAX_LL ? LOGN : ROW_MAX_LL;  // residues per CTA = 2^LL
+    static constexpr int SP = 1 << (LOGN - LL);                      // CTAs per row
+    static constexpr bool SPLIT = SP > 1;
     static constexpr int N = 1 << LOGN;
+    static_assert(SP <= 4, "rows are split over at most 4 CTAs");
 };
 template <int LOGN, int E = 16>
 constexpr int KT = ntt::Shape<Row<LOGN>::LL, E>::T;
 template <int LOGN>
 __device__ __forceinline__ int lbx() {
-    return Row<LOGN>::SPLIT ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    return (int)blockIdx.x / Row<LOGN>::SP;
 }
 template <int LOGN>
-__device__ __forceinline__ int rhalf() {
-    return Row<LOGN>::SPLIT ? (int)(blockIdx.x & 1) : 0;
+__device__ __forceinline__ int rpart() {
+    return (int)blockIdx.x % Row<LOGN>::SP;
 }
 template <int LOGN, int E = 16>
 __device__ __forceinline__ int tpos() {
-    return (rhalf<LOGN>() << Row<LOGN>::LL) + 2 * (int)threadIdx.x;
+    return (rpart<LOGN>() << Row<LOGN>::LL) + 2 * (int)threadIdx.x;
 }
 // HEB_PATH_PROBE (build experiments only): 1 = FP64 engine only, 2 = integer engine only
 #if defined(HEB_PATH_PROBE) && HEB_PATH_PROBE == 1
@@ -228,7 +233,7 @@ __device__ __forceinline__ void fwd_any(const Ctx &K, int row, const PrimeInfo &
     if constexpr (ENG == 2) {
         const ntt::IntArith ar(P.p);
         const ulonglong2 *tw = K.tw + ((size_t)row << LOGN);
-        if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, E>(ar, sm, tw, load, out, rhalf<LOGN>());
+        if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, E, Row<LOGN>::SP>(ar, sm, tw, load, out, rpart<LOGN>());
         else ntt::forward<LL, E>(ar, sm, tw, load, out);
         return;
     }
@@ -236,12 +241,12 @@ __device__ __forceinline__ void fwd_any(const Ctx &K, int row, const PrimeInfo &
         const ntt::FpArith ar(P.pd, P.pinvd);
         double *s = reinterpret_cast<double *>(sm);
         const double *tw = K.twf + ((size_t)row << LOGN);
-        if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, E>(ar, s, tw, load, out, rhalf<LOGN>());
+        if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, E, Row<LOGN>::SP>(ar, s, tw, load, out, rpart<LOGN>());
         else ntt::forward<LL, E>(ar, s, tw, load, out);
     } else if constexpr (ENG == 0) {
         const ntt::IntArith ar(P.p);
         const ulonglong2 *tw = K.tw + ((size_t)row << LOGN);
-        if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, E>(ar, sm, tw, load, out, rhalf<LOGN>());
+        if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, E, Row<LOGN>::SP>(ar, sm, tw, load, out, rpart<LOGN>());
         else ntt::forward<LL, E>(ar, sm, tw, load, out);
     }
 }
@@ -255,7 +260,7 @@ __device__ __forceinline__ void inv_any(const Ctx &K, int row, const PrimeInfo &
         const ntt::IntArith ar(P.p);
         const ulonglong2 *itw = K.itw + ((size_t)row << LOGN);
         const ulonglong2 u = std_out ? lc.u_std : lc.u_plain, v = std_out ? lc.v_std : lc.v_plain;
-        if constexpr (Row<LOGN>::SPLIT) ntt::inverse_split<LL, E>(ar, sm, itw, in, store, u, v, rhalf<LOGN>());
+        if constexpr (Row<LOGN>::SPLIT) ntt::inverse_split<LL, E, Row<LOGN>::SP>(ar, sm, itw, in, store, u, v, rpart<LOGN>());
         else ntt::inverse<LL, E>(ar, sm, itw, in, store, u, v);
         return;
     }
@@ -264,22 +269,22 @@ __device__ __forceinline__ void inv_any(const Ctx &K, int row, const PrimeInfo &
         double *s = reinterpret_cast<double *>(sm);
         const double *itw = K.itwf + ((size_t)row << LOGN);
         const double u = std_out ? lc.fu_std : lc.fu_plain, v = std_out ? lc.fv_std : lc.fv_plain;
-        if constexpr (Row<LOGN>::SPLIT) ntt::inverse_split<LL, E>(ar, s, itw, in, store, u, v, rhalf<LOGN>());
+        if constexpr (Row<LOGN>::SPLIT) ntt::inverse_split<LL, E, Row<LOGN>::SP>(ar, s, itw, in, store, u, v, rpart<LOGN>());
         else ntt::inverse<LL, E>(ar, s, itw, in, store, u, v);
     } else if constexpr (ENG == 0) {
         const ntt::IntArith ar(P.p);
         const ulonglong2 *itw = K.itw + ((size_t)row << LOGN);
         const ulonglong2 u = std_out ? lc.u_std : lc.u_plain, v = std_out ? lc.v_std : lc.v_plain;
-        if constexpr (Row<LOGN>::SPLIT) ntt::inverse_split<LL, E>(ar, sm, itw, in, store, u, v, rhalf<LOGN>());
+        if constexpr (Row<LOGN>::SPLIT) ntt::inverse_split<LL, E, Row<LOGN>::SP>(ar, sm, itw, in, store, u, v, rpart<LOGN>());
         else ntt::inverse<LL, E>(ar, sm, itw, in, store, u, v);
     }
 }
 
-// Launch a row kernel: split rows get twice the CTAs along x, clustered in pairs.
+// Launch a row kernel: split rows get SP times the CTAs along x, clustered SP at a time.
 template <int LOGN, class Kern, class... Args>
 static cudaError_t launch_rows(Kern kernel, dim3 grid, int block, size_t smem, cudaStream_t st, Args... args) {
     if constexpr (Row<LOGN>::SPLIT) {
-        grid.x *= 2;
+        grid.x *= Row<LOGN>::SP;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = grid;
         cfg.blockDim = dim3(block);
@@ -287,7 +292,7 @@ static cudaError_t launch_rows(Kern kernel, dim3 grid, int block, size_t smem, c
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.x = Row<LOGN>::SP;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;

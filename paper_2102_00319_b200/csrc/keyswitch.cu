@@ -142,11 +142,11 @@ struct DigitLoad {
     bool small;
     __device__ __forceinline__ DigitLoad(const i64 *d_, const PrimeInfo &P, u64 qj)
         : d(d_), p(P.p), r1s(P.r1s), small((qj >> 1) < P.p) {}
-    __device__ __forceinline__ u64 operator()(int i) const {
-        const i64 v = __ldcg(d + i);
+    __device__ __forceinline__ u64 conv(i64 v) const {
         if (small) return (u64)v + (v < 0 ? p : 0);
         return signed_mul_const(v, 1, r1s, p);
     }
+    __device__ __forceinline__ u64 operator()(int i) const { return conv(__ldcg(d + i)); }
 };
 
 template <int LOGN>
@@ -303,6 +303,9 @@ __device__ __forceinline__ void modup_store(uint32_t ta, u64 *o0, u64 *o1, int p
 #ifndef MODUP_STAGE
 #define MODUP_STAGE 1
 #endif
+#ifndef MODUP_STAGE_INT
+#define MODUP_STAGE_INT 1
+#endif
 template <int LL>
 __device__ __forceinline__ void stage_row_async(u64 *sm, const i64 *src) {
     constexpr int N = 1 << LL;
@@ -346,17 +349,47 @@ __host__ __device__ constexpr uint32_t modup_tmem_cols() {
 #ifndef MODUP_FP_MINB
 #define MODUP_FP_MINB(LOGN) NTT_MINB(LOGN)
 #endif
+// L2 prefetch of this CTA's part of key row (j, gt) (b and a parts): the key products of a
+// digit follow its transform, so the key is in L2 by then (cfg4: 160 MB of key, larger
+// than L2, re-read for every item).
+template <int LOGN, bool FP>
+__device__ __forceinline__ void prefetch_key(const ulonglong2 *keyrow) {
+    constexpr int LL = Row<LOGN>::LL;
+    constexpr uint32_t bytes = (1u << LL) * (FP ? 8u : 16u);
+    const size_t stride = (size_t)(1 << LOGN) * (FP ? 8 : 16);
+    const char *base = FP ? reinterpret_cast<const char *>(reinterpret_cast<const double *>(keyrow) + (rpart<LOGN>() << LL))
+                          : reinterpret_cast<const char *>(keyrow + (rpart<LOGN>() << LL));
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + c * stride), "r"(bytes) : "memory");
+}
+
+// Targets of one fused-ModUp launch (each NTT engine gets its own launch and list).
+struct TargetList {
+    int n;
+    signed char t[60];
+};
+
+#ifndef MODUP_STAGE_SPLIT
+#define MODUP_STAGE_SPLIT 0
+#endif
+#ifndef MODUP_KEY_PREFETCH
+#define MODUP_KEY_PREFETCH 0
+#endif
+// Launch order: logical x = target index * G + item-in-group, y = item group.  CTAs are
+// dispatched x-fastest, so each group of G items runs target by target: a target's key
+// rows are shared (in L2) by the G items' CTAs while the group's digits stay in L2.
 template <int LOGN, int ENG>
 __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MODUP_FP_MINB(LOGN)) k_ks_modup_fused(Ctx K, heb_ct src, int comp, const i64 *D, const ulonglong2 *key,
-                                                  int k, u64 *acc, int64_t count) {
+                                                  int k, u64 *acc, int64_t count, TargetList tl, int G) {
     extern __shared__ u64 sm[];
     __shared__ uint32_t tbase;
+    // one (item, target) per CTA (pair): the host sizes the grid to cover every item
+    const int L = lbx<LOGN>();
+    const int ti = L / G;
+    const int64_t b = (int64_t)blockIdx.y * G + (L - ti * G);
+    if (b >= count) return;  // both CTAs of a cluster agree
     const int warp = threadIdx.x >> 5;
-    if (ENG != 0) {
-        const int xi0 = lbx<LOGN>();
-        const int t0 = xi0 == 0 ? 0 : (xi0 == (k + 1) / 2 ? k : (xi0 < (k + 1) / 2 ? xi0 : xi0 - 1));
-        if (K.pi[t0 < k ? t0 : K.num_rows - 1].use_fp != (ENG == 1)) return;
-    }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          (uint32_t)__cvta_generic_to_shared(&tbase)),
@@ -369,18 +402,27 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t ta = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
 
-    // targets in an interleaved order: the two wide (integer) targets 0 and k are spread
-    // between the narrow ones so co-resident CTAs mix IMAD- and DFMA-bound work
-    const int xi = lbx<LOGN>();
-    const int t = xi == 0 ? 0 : (xi == (k + 1) / 2 ? k : (xi < (k + 1) / 2 ? xi : xi - 1));
+    const int t = tl.t[ti];
     const int gt = t < k ? t : K.num_rows - 1;
     const PrimeInfo P = K.pi[gt];
     const int n = 1 << LOGN, R = K.num_rows;
     const int pos = tpos<LOGN>();
-    for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
+    constexpr int LL = Row<LOGN>::LL;
+    const int hoff = rpart<LOGN>() << LL;  // this CTA's first position (split rows: part r)
+    {
         bool first = true;
-        int staged_for = -1;  // digit whose row sits in shared memory (MODUP_STAGE)
+        int staged_for = -1;  // digit whose row (this CTA's part) sits in shared memory
+        if constexpr (Row<LOGN>::SPLIT && MODUP_STAGE_SPLIT && ENG != 0) {
+            // split rows only ever transform from staged digits: stage the first one now
+            const int j0 = t == 0 ? 1 : 0;
+            if (j0 < k) {
+                stage_row_async<LL>(sm, D + (b * k + j0) * n + hoff);
+                staged_for = j0;
+            }
+        }
         for (int j = 0; j < k; ++j) {
+            if (MODUP_KEY_PREFETCH && ENG != 0 && threadIdx.x == 0)
+                prefetch_key<LOGN, ENG == 1>(key + (((size_t)j * R + gt) * 2) * n);
             u64 y[16];
             if (j == t) {
                 load16<LOGN>(at(src, b, comp, t, LOGN) + pos, y);  // d2_t: congruent digit, no transform
@@ -394,63 +436,52 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
                 if constexpr (ENG == 0) {
                     fwd_any<LOGN>(K, gt, P, sm, ld, y);
                 } else {
-                    constexpr int LL = Row<LOGN>::LL;
+                    const bool staged = staged_for == j;
                     if constexpr (ENG == 1) {
                         const ntt::FpArithRaw ar(P.pd, P.pinvd);
                         double *s2 = reinterpret_cast<double *>(sm);
                         const double *tw = K.twf + ((size_t)gt << LOGN);
                         if constexpr (Row<LOGN>::SPLIT) {
-                            ntt::forward_split<LL, 16>(ar, s2, tw, ld, y, rhalf<LOGN>());
-                        } else if (MODUP_STAGE && staged_for == j) {
+                            if constexpr (MODUP_STAGE_SPLIT) ntt::forward_split_staged<LL, 16, Row<LOGN>::SP>(ar, s2, tw, ld, y, rpart<LOGN>());
+                            else ntt::forward_split<LL, 16, Row<LOGN>::SP>(ar, s2, tw, ld, y, rpart<LOGN>());
+                        } else if (MODUP_STAGE && staged) {
                             asm volatile("cp.async.wait_all;" ::: "memory");
                             __syncthreads();
                             first_group_positions<LL>([&](int i) {
                                 const int q = ntt::pad(i);
-                                const i64 v = reinterpret_cast<const i64 *>(sm)[q];
-                                const u64 c = ld.small ? (u64)v + (v < 0 ? ld.p : 0) : signed_mul_const(v, 1, ld.r1s, ld.p);
-                                s2[q] = ntt::u2d(c);
+                                s2[q] = ntt::u2d(ld.conv(reinterpret_cast<const i64 *>(sm)[q]));
                             });
                             ntt::forward_core<LL, 16, true>(ar, s2, tw, 1, ld, y);
                         } else {
                             ntt::forward<LL, 16>(ar, s2, tw, ld, y);
                         }
-                        if constexpr (MODUP_STAGE && !Row<LOGN>::SPLIT) {
-                            int jn = j + 1;
-                            if (jn == t) ++jn;
-                            if (jn < k) {
-                                __syncthreads();  // every thread has read the transform's output
-                                stage_row_async<LL>(sm, D + (b * k + jn) * n);
-                                staged_for = jn;
-                            }
-                        }
                     } else {
                         const ntt::IntArith ar(P.p);
                         const ulonglong2 *tw = K.tw + ((size_t)gt << LOGN);
-#ifndef MODUP_STAGE_INT
-#define MODUP_STAGE_INT 1
-#endif
                         if constexpr (Row<LOGN>::SPLIT) {
-                            ntt::forward_split<LL, 16>(ar, sm, tw, ld, y, rhalf<LOGN>());
-                        } else if (MODUP_STAGE_INT && staged_for == j) {
+                            if constexpr (MODUP_STAGE_SPLIT) ntt::forward_split_staged<LL, 16, Row<LOGN>::SP>(ar, sm, tw, ld, y, rpart<LOGN>());
+                            else ntt::forward_split<LL, 16, Row<LOGN>::SP>(ar, sm, tw, ld, y, rpart<LOGN>());
+                        } else if (MODUP_STAGE_INT && staged) {
                             asm volatile("cp.async.wait_all;" ::: "memory");
                             __syncthreads();
                             first_group_positions<LL>([&](int i) {
                                 const int q = ntt::pad(i);
-                                const i64 v = reinterpret_cast<const i64 *>(sm)[q];
-                                sm[q] = ld.small ? (u64)v + (v < 0 ? ld.p : 0) : signed_mul_const(v, 1, ld.r1s, ld.p);
+                                sm[q] = ld.conv(reinterpret_cast<const i64 *>(sm)[q]);
                             });
                             ntt::forward_core<LL, 16, true>(ar, sm, tw, 1, ld, y);
                         } else {
                             ntt::forward<LL, 16>(ar, sm, tw, ld, y);
                         }
-                        if constexpr (MODUP_STAGE_INT && !Row<LOGN>::SPLIT) {
-                            int jn = j + 1;
-                            if (jn == t) ++jn;
-                            if (jn < k) {
-                                __syncthreads();
-                                stage_row_async<LL>(sm, D + (b * k + jn) * n);
-                                staged_for = jn;
-                            }
+                    }
+                    // stage the next digit's row (this CTA's part) during the key products
+                    constexpr bool stage_on = Row<LOGN>::SPLIT ? MODUP_STAGE_SPLIT : (ENG == 1 ? MODUP_STAGE : MODUP_STAGE_INT);
+                    if constexpr (stage_on) {
+                        int jn = j + 1;
+                        if (jn == t) ++jn;
+                        if (jn < k) {
+                            __syncthreads();  // every thread has read the transform's output
+                            stage_row_async<LL>(sm, D + (b * k + jn) * n + hoff);
+                            staged_for = jn;
                         }
                     }
                 }
@@ -735,7 +766,7 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_down_rescale_tail(Ctx K, const u64 *acc, h
                 return (u64)__double_as_longlong(v);
             };
             constexpr int LL = Row<LOGN>::LL;
-            if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, 16>(fa, s2, twf, ld, y, rhalf<LOGN>());
+            if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, 16, Row<LOGN>::SP>(fa, s2, twf, ld, y, rpart<LOGN>());
             else ntt::forward<LL, 16>(fa, s2, twf, ld, y);
             u64 x[16], z[16];
             load16<LOGN>(acc + ((b * 2 + c) * (k + 1) + i) * n + pos, x);
@@ -854,6 +885,23 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
 #ifndef MODUP_ENGINES_SPLIT
 #define MODUP_ENGINES_SPLIT 1
 #endif
+            // each engine's launch covers exactly its own targets (no early-exit CTAs);
+            // G items per group, targets in sequence within a group (see the kernel)
+            TargetList tl_fp{0, {}}, tl_int{0, {}}, tl_all{0, {}};
+            for (int t = 0; t <= k; ++t) {
+                const int gt = t < k ? t : c->num_rows - 1;
+                TargetList &l = c->row_fp[gt] ? tl_fp : tl_int;
+                l.t[l.n++] = (signed char)t;
+                tl_all.t[tl_all.n++] = (signed char)t;
+            }
+            static const int G_env = [] {
+                const char *e = getenv("HEB_MODUP_G");
+                return e ? std::max(1, atoi(e)) : 0;
+            }();
+            // every (item, target) gets its own CTA (pair): G * 65535 >= cnt
+            const int G = (int)std::min<int64_t>(
+                cnt, std::max<int64_t>((cnt + 65534) / 65535, G_env > 0 ? G_env : 1));
+            const unsigned gyg = (unsigned)((cnt + G - 1) / G);
             if (MODUP_ENGINES_SPLIT) {
                 // the integer-target and FP64-target launches are independent (disjoint acc
                 // rows): the integer one goes to the stream's side stream so their CTAs share
@@ -863,15 +911,17 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
                     return !(e && *e == '0');
                 }();
                 cudaStream_t ist = st;
-                if (concurrent) CUDA_TRY(side_fork(c, st, &ist));
-                CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 2>, dim3(dim3(k + 1, gy)), KT<LOGN>, sm, ist, K, s,
-                                           comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt));
-                CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 1>, dim3(dim3(k + 1, gy)), KT<LOGN>, sm, st, K, s,
-                                           comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt));
-                if (concurrent) CUDA_TRY(side_join(c, st));
+                if (concurrent && tl_int.n) CUDA_TRY(side_fork(c, st, &ist));
+                if (tl_int.n)
+                    CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 2>, dim3(tl_int.n * G, gyg), KT<LOGN>, sm, ist, K,
+                                               s, comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt, tl_int, G));
+                if (tl_fp.n)
+                    CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 1>, dim3(tl_fp.n * G, gyg), KT<LOGN>, sm, st, K,
+                                               s, comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt, tl_fp, G));
+                if (concurrent && tl_int.n) CUDA_TRY(side_join(c, st));
             } else {
-                CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 0>, dim3(dim3(k + 1, gy)), KT<LOGN>, sm, st, K, s,
-                                           comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt));
+                CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 0>, dim3(tl_all.n * G, gyg), KT<LOGN>, sm, st, K, s,
+                                           comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt, tl_all, G));
             }
         }
         for (int64_t s0 = 0; s0 < (fused ? 0 : cnt); s0 += sub) {

@@ -23,16 +23,16 @@
 //             costs ~8 IMAD-pipe slots (tools/pipes_bench.cu).  A product mod p is 6
 //             exact FP64 ops; values stay unreduced and signed between stages (< 2^47).
 //
-// N = 2^15 rows do not fit one CTA's shared memory; they run on a 2-CTA cluster
-// (forward_split / inverse_split): the only cross-half stage (s = 0) is folded into
-// the forward's loads (each CTA reads both halves) and into the inverse's epilogue
-// (each CTA reads the peer's half through distributed shared memory).  Within a half,
-// stage s' of the local transform uses global twiddle (2 + h) * 2^s' + block, so the
-// same engine runs with a twiddle base multiplier c0 = 2 + h (c0 = 1 otherwise).
+// Rows longer than one CTA's part (2^LL, see Row in common.cuh) run on an SP-CTA cluster
+// (SP = 2 or 4; forward_split / inverse_split): the log2(SP) cross-part stages work
+// column-wise over the parts' shared memories (distributed shared memory), the rest is
+// local.  Within part r, stage s' of the local transform uses global twiddle
+// (SP + r) * 2^s' + block, so the same engine runs with a twiddle base multiplier
+// c0 = SP + r (c0 = 1 otherwise).
 //
 // Interfaces chosen so that callers can fuse prologues/epilogues:
 //   forward: input through a functor load(idx) (coalesced across threads), output
-//            left in registers in line-pair order (lpos below) of its row (of its half
+//            left in registers in line-pair order (lpos below) of its row (of its part
 //            for split rows);
 //   inverse: input given in registers in that same layout, output through a functor
 //            store(idx, value) (coalesced).
@@ -94,10 +94,6 @@ struct IntArith {
     HD u64 out_fwd(V x) const { return csub(csub(x, p2), p); }
     HD u64 out_inv(V x) const { return x; }
     HD V to_smem_inv(V x) const { return x; }
-    HD V split_fwd(V a, V b, W w1, int h) const {  // stage 0 for half h, a,b in [0,2p)
-        const u64 t = shoup_lazy(b, w1.x, w1.y, p);
-        return h ? a - t + p2 : a + t;
-    }
 };
 
 #define FP_MAGIC 6755399441055744.0  // 1.5 * 2^52
@@ -150,10 +146,6 @@ struct FpArith {
     HD u64 out_inv(V x) const { return fcanon(x, p, pinv); }
     // the inverse's additive path grows by up to 2^RB per group: re-centre at exchanges
     HD V to_smem_inv(V x) const { return fred(x, p, pinv); }
-    HD V split_fwd(V a, V b, W w1, int h) const {
-        const double r = fmul(b, w1, p, pinv);
-        return h ? a - r : a + r;
-    }
 };
 
 // FP64 engine whose forward hands out raw (unreduced, signed, |v| < 2^47) doubles as bit
@@ -257,19 +249,113 @@ __device__ void forward(const A &ar, typename A::V *sm, const typename A::W *__r
     forward_core<LOGN, E, false>(ar, sm, tw, 1, load, out);
 }
 
-// Forward NTT of a 2^(LL+1) row split over a 2-CTA cluster; this CTA (half h) ends
-// with positions h*2^LL + E t .. + E-1 in registers.  load(idx) takes global indices.
-template <int LL, int E = 16, class A, class Load>
-__device__ void forward_split(const A &ar, typename A::V *sm, const typename A::W *__restrict__ tw, Load load,
-                              u64 (&out)[E], int h) {
-    using S = Shape<LL, E>;
-    __syncthreads();
+// Cross-CTA stages of a row split over SP = 2 or 4 CTAs (x[q] = the element of part q at
+// one local index j): the first log2(SP) forward stages (CT), in place.
+template <int SP, class A>
+HD void cross_fwd(const A &ar, typename A::V (&x)[SP], const typename A::W *__restrict__ tw) {
+    static_assert(SP == 2 || SP == 4, "2- or 4-CTA rows");
     const auto w1 = __ldg(tw + 1);
-    constexpr int half = 1 << LL;
-    for (int j = threadIdx.x; j < half; j += S::T)
-        sm[pad(j)] = ar.split_fwd(ar.in(load(j)), ar.in(load(j + half)), w1, h);
+    if constexpr (SP == 2) {
+        ar.fwd(x[0], x[1], w1);
+    } else {
+        ar.fwd(x[0], x[2], w1);
+        ar.fwd(x[1], x[3], w1);
+        ar.fwd(x[0], x[1], __ldg(tw + 2));
+        ar.fwd(x[2], x[3], __ldg(tw + 3));
+    }
+}
+
+// Forward NTT of a 2^LL * SP row split over an SP-CTA cluster (this CTA: part r).  Each
+// CTA brings its own part into shared memory (load(idx) with global indices), then the
+// cross-part stages run column-wise through distributed shared memory -- CTA r owns local
+// columns [r C, (r+1) C), C = 2^LL / SP, reading the column's SP elements (one local) and
+// writing them back, so every location has one reader/writer -- and the rest of the
+// transform is local (global stage s = log2(SP) + s' uses twiddle (SP + r) 2^s' + block).
+// Ends with positions r 2^LL + lpos(t, m) in registers.
+template <int LL, int E, int SP, class A>
+__device__ void split_cross_and_local(const A &ar, typename A::V *sm, const typename A::W *__restrict__ tw,
+                                      u64 (&out)[E], int r) {
+    using S = Shape<LL, E>;
+    using V = typename A::V;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();  // every part is in its CTA's shared memory
+    V *parts[SP];
+#pragma unroll
+    for (int q = 0; q < SP; ++q) parts[q] = cluster.map_shared_rank(sm, q);
+    constexpr int C = (1 << LL) / SP;
+#pragma unroll 2
+    for (int j = r * C + (int)threadIdx.x; j < (r + 1) * C; j += S::T) {
+        const int i = pad(j);
+        V x[SP];
+#pragma unroll
+        for (int q = 0; q < SP; ++q) x[q] = parts[q][i];
+        cross_fwd<SP>(ar, x, tw);
+#pragma unroll
+        for (int q = 0; q < SP; ++q) parts[q][i] = x[q];
+    }
+    cluster.sync();  // every column written
+    int dummy = 0;
+    auto noload = [&](int) { return (u64)dummy; };
+    forward_core<LL, E, true>(ar, sm, tw, SP + r, noload, out);
+}
+
+// Cross-part stages for one CTA's own output only (part r of SP): 1 (SP = 2) or 3
+// (SP = 4) products per element instead of a full column.
+template <int SP, class A>
+HD typename A::V cross_fwd_part(const A &ar, typename A::V (&x)[SP], const typename A::W *__restrict__ tw, int r) {
+    const auto w1 = __ldg(tw + 1);
+    if constexpr (SP == 2) {
+        ar.fwd(x[0], x[1], w1);
+        return r ? x[1] : x[0];
+    } else {
+        const int h = r >> 1;
+        ar.fwd(x[0], x[2], w1);
+        ar.fwd(x[1], x[3], w1);
+        typename A::V y0 = h ? x[2] : x[0], y1 = h ? x[3] : x[1];
+        ar.fwd(y0, y1, __ldg(tw + 2 + h));
+        return (r & 1) ? y1 : y0;
+    }
+}
+
+// Forward NTT of a 2^LL * SP row split over SP CTAs (this CTA: part r), without any
+// cross-CTA synchronisation: each CTA reads the SP elements of every one of its columns
+// from global memory (load(idx) takes global indices), forms its own part of the
+// cross-part stages, then runs the local stages.
+template <int LL, int E = 16, int SP = 2, class A, class Load>
+__device__ void forward_split(const A &ar, typename A::V *sm, const typename A::W *__restrict__ tw, Load load,
+                              u64 (&out)[E], int r) {
+    using S = Shape<LL, E>;
+    using V = typename A::V;
+    __syncthreads();  // shared memory may still be read by a previous transform
+    constexpr int PER = (1 << LL) / S::T;
+#pragma unroll 4
+    for (int k = 0; k < PER; ++k) {
+        const int j = (int)threadIdx.x + k * S::T;
+        V x[SP];
+#pragma unroll
+        for (int q = 0; q < SP; ++q) x[q] = ar.in(load((q << LL) + j));
+        sm[pad(j)] = cross_fwd_part<SP>(ar, x, tw, r);
+    }
     __syncthreads();
-    forward_core<LL, E, true>(ar, sm, tw, 2 + h, load, out);
+    forward_core<LL, E, true>(ar, sm, tw, SP + r, load, out);
+}
+
+// The same transform when this CTA's part was staged into shared memory as raw 64-bit
+// words by cp.async (thread t copied positions t, t + T, ...): each thread converts its
+// own copies in place (conv.conv(raw) -> residue) once they have landed.
+template <int LL, int E = 16, int SP = 2, class A, class Conv>
+__device__ void forward_split_staged(const A &ar, typename A::V *sm, const typename A::W *__restrict__ tw,
+                                     const Conv &conv, u64 (&out)[E], int r) {
+    using S = Shape<LL, E>;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    const long long *raw = reinterpret_cast<const long long *>(sm);
+#pragma unroll 4
+    for (int j = threadIdx.x; j < (1 << LL); j += S::T) {
+        const int i = pad(j);
+        sm[i] = ar.in(conv.conv(raw[i]));
+    }
+    split_cross_and_local<LL, E, SP>(ar, sm, tw, out, r);
 }
 
 // ---------------------------------------------------------------- inverse ----
@@ -370,31 +456,51 @@ __device__ void inverse(const A &ar, typename A::V *sm, const typename A::W *__r
     inverse_core<LOGN, E, false>(ar, sm, itw, 1, in, store, last_u, last_v);
 }
 
-// Inverse NTT of a 2^(LL+1) row over a 2-CTA cluster (half h supplies positions
-// h*2^LL + E t ..); store() receives global indices.  Stage 0 pairs (j, j + 2^LL)
-// across the halves: CTA h finishes j in [h 2^(LL-1), (h+1) 2^(LL-1)) reading the
-// peer half from distributed shared memory.
-template <int LL, int E = 16, class A, class Store>
+// Last log2(SP) inverse stages of a split row (GS, global stages log2(SP)-1 .. 0; the
+// final one folds n^-1 and the caller's output factor: inv_last with last_u / last_v).
+template <int SP, class A>
+HD void cross_inv(const A &ar, typename A::V (&x)[SP], const typename A::W *__restrict__ itw, typename A::W last_u,
+                  typename A::W last_v) {
+    static_assert(SP == 2 || SP == 4, "2- or 4-CTA rows");
+    if constexpr (SP == 2) {
+        ar.inv_last(x[0], x[1], last_u, last_v);
+    } else {
+        ar.inv(x[0], x[1], __ldg(itw + 2));
+        ar.inv(x[2], x[3], __ldg(itw + 3));
+        ar.inv_last(x[0], x[2], last_u, last_v);
+        ar.inv_last(x[1], x[3], last_u, last_v);
+    }
+}
+
+// Inverse NTT of a 2^LL * SP row over an SP-CTA cluster (part r supplies positions
+// r 2^LL + lpos(t, m)).  The local stages run first (results left in shared memory), then
+// CTA r finishes local columns [r C, (r+1) C) across all parts through distributed shared
+// memory and stores all SP outputs of each column: store(idx, v) gets global indices.
+template <int LL, int E = 16, int SP = 2, class A, class Store>
 __device__ void inverse_split(const A &ar, typename A::V *sm, const typename A::W *__restrict__ itw,
-                              const u64 (&in)[E], Store store, typename A::W last_u, typename A::W last_v, int h) {
+                              const u64 (&in)[E], Store store, typename A::W last_u, typename A::W last_v, int r) {
     using S = Shape<LL, E>;
     using V = typename A::V;
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     __syncthreads();
-    inverse_core<LL, E, true>(ar, sm, itw, 2 + h, in, store, last_u, last_v);
+    inverse_core<LL, E, true>(ar, sm, itw, SP + r, in, store, last_u, last_v);
     cluster.sync();
-    V *peer = cluster.map_shared_rank(sm, h ^ 1);
-    const V *s0 = h ? peer : sm;
-    const V *s1 = h ? sm : peer;
-    constexpr int half = 1 << LL, quarter = half >> 1;
-    for (int j = h * quarter + threadIdx.x; j < (h + 1) * quarter; j += S::T) {
-        V a = s0[pad(j)], b = s1[pad(j)];
-        ar.inv_last(a, b, last_u, last_v);
-        store(j, ar.out_inv(a));
-        store(j + half, ar.out_inv(b));
+    const V *parts[SP];
+#pragma unroll
+    for (int q = 0; q < SP; ++q) parts[q] = cluster.map_shared_rank(sm, q);
+    constexpr int C = (1 << LL) / SP;
+#pragma unroll 2
+    for (int j = r * C + (int)threadIdx.x; j < (r + 1) * C; j += S::T) {
+        const int i = pad(j);
+        V x[SP];
+#pragma unroll
+        for (int q = 0; q < SP; ++q) x[q] = parts[q][i];
+        cross_inv<SP>(ar, x, itw, last_u, last_v);
+#pragma unroll
+        for (int q = 0; q < SP; ++q) store((q << LL) + j, ar.out_inv(x[q]));
     }
-    cluster.sync();  // the peer must not reuse its shared memory while it is being read
+    cluster.sync();  // the peers must not reuse their shared memory while it is being read
 }
 
 }  // namespace ntt

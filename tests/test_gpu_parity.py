@@ -237,9 +237,10 @@ def test_batched_layers_match_reference(golden, dev_s128, name, fused):
     assert np.allclose(dec[:, :8].T, np.array(g["decrypted_first8"]), atol=0, rtol=0)
 
 
-@pytest.mark.parametrize("logn", [15])
+@pytest.mark.parametrize("logn", [14, 15])
 def test_ntt_split_rows_match_oracle(logn):
-    """N = 2^15 rows run on a 2-CTA cluster (DSMEM cross-half stage)."""
+    """N = 2^14 / 2^15 rows run on 2- / 4-CTA clusters (cross-part stages through
+    distributed shared memory)."""
     from oracle import ckks_oracle as oc
     from paper_2102_00319_b200.backend import DeviceContext, u64_to_dev, dev_to_u64
     from paper_2102_00319_b200.chain import build_chain
