@@ -15,8 +15,10 @@
  *   Rows are the prefix 0..level of the context's primes (row 0 = base prime).
  *   Raw products (degree 2) use the same descriptor with three components.
  * All work is enqueued on `stream` (a cudaStream_t, may be NULL); temporary
- * device memory is stream-ordered (cudaMallocAsync), so independent calls may
- * use independent streams.
+ * device memory comes from a per-stream scratch arena owned by the context (LIFO bump
+ * allocation over device blocks that only grow during the first calls of a shape), so
+ * independent calls may use independent streams and CUDA-graph replays touch no
+ * allocator.  One host thread at a time per stream (a lock per arena serialises).
  */
 #ifndef HEB200_H
 #define HEB200_H
@@ -56,11 +58,15 @@ int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows, const uin
 int heb_ctx_destroy(heb_ctx *ctx);
 int heb_ctx_ring_degree(const heb_ctx *ctx);
 /* Key-switch / rescale batches are processed in chunks of this many items
- * (default 1024), bounding the stream-ordered scratch. */
+ * (default 1024), bounding the scratch arena. */
 int heb_ctx_set_chunk(heb_ctx *ctx, int items);
 /* Free the scratch arena of `stream` (after synchronising it); the next call on that
- * stream grows a new one.  For one-off evaluations on streams that will not be reused. */
+ * stream grows a new one.  For one-off evaluations on streams that will not be reused.
+ * Refused (HEB_EINVAL) while CUDA graphs captured on `stream` may replay into the arena:
+ * destroy them first, then heb_ctx_clear_captured. */
 int heb_ctx_release_scratch(heb_ctx *ctx, void *stream);
+/* Declare that no CUDA graph captured on `stream` is alive any more. */
+int heb_ctx_clear_captured(heb_ctx *ctx, void *stream);
 
 /* --- memory ----------------------------------------------------------------- */
 int heb_alloc(size_t bytes, void **out, void *stream);

@@ -25,7 +25,9 @@ math of the reference ``CkksBackend``
 Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU legs may
 import this module.  It uses the product's host-only helpers (chain tables,
 samplers, FFT encoding), which are themselves pinned against the reference's
-golden vectors in ``tests/test_host_golden.py``.
+golden vectors in ``tests/test_oracle_golden.py`` (fixtures from
+``tests/golden/make_golden.py``) and ``tests/test_canonical.py`` (the reference's
+own ``run_inference`` and BASELINE-size op digests, ``tests/golden/make_canonical.py``).
 """
 
 from __future__ import annotations

@@ -37,6 +37,7 @@ SIGNATURES: dict[str, list] = {
     "heb_ctx_ring_degree": [_P],
     "heb_ctx_set_chunk": [_P, _I],
     "heb_ctx_release_scratch": [_P, _P],
+    "heb_ctx_clear_captured": [_P, _P],
     "heb_alloc": [ctypes.c_size_t, ctypes.POINTER(_P), _P],
     "heb_free": [_P, _P],
     "heb_h2d": [_P, _P, ctypes.c_size_t, _P],

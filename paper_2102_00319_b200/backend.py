@@ -89,14 +89,21 @@ class DeviceContext:
         return torch.empty(shape, dtype=torch.int64, device=self.device)
 
     def call(self, name: str, *args) -> None:
+        # every entry point runs on this context's device (scratch allocations, kernel
+        # attributes and launches follow the calling thread's current device)
+        if torch.cuda.current_device() != self.device.index:
+            with torch.cuda.device(self.device):
+                _lib.call(name, self.handle, *args)
+            return
         _lib.call(name, self.handle, *args)
 
     def set_chunk(self, items: int) -> None:
-        _lib.call("heb_ctx_set_chunk", self.handle, items)
+        self.call("heb_ctx_set_chunk", items)
 
     def release_scratch(self, stream=None) -> None:
-        """Free the scratch arena of ``stream`` (default: this context's stream)."""
-        _lib.call("heb_ctx_release_scratch", self.handle, self.stream if stream is None else stream)
+        """Free the scratch arena of ``stream`` (default: this context's stream).  Refused
+        (DeviceError) while CUDA graphs captured on that stream may replay into it."""
+        self.call("heb_ctx_release_scratch", self.stream if stream is None else stream)
 
     def __del__(self):
         h = getattr(self, "handle", None)

@@ -41,8 +41,9 @@ class LogitGather:
         stream is ordered after the gather.  Collectives of one communicator must run in
         the same order on every rank, so all of them go through one communication stream
         even when several pipelines (streams) produce logits."""
-        src = logits.contiguous()
-        st = stream if stream is not None else torch.cuda.current_stream(src.device)
+        st = stream if stream is not None else torch.cuda.current_stream(logits.device)
+        with torch.cuda.stream(st):  # the copy (if any) is ordered after the producer's work
+            src = logits.contiguous()
         if self._comm_stream is None:
             self._comm_stream = torch.cuda.Stream(src.device)
         cs = self._comm_stream

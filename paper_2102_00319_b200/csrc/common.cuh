@@ -81,6 +81,9 @@ struct StreamArena {
     cudaStream_t side = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     size_t blk = 0, off = 0;  // bump position
+    // set when scratch was handed out during a CUDA-graph capture on this stream: the
+    // graph holds raw block addresses, so the blocks must outlive it
+    bool captured = false;
 };
 
 struct heb_ctx {
@@ -114,10 +117,13 @@ struct heb_ctx {
 struct Scratch {
     void *p = nullptr;
     StreamArena *a;
+    cudaStream_t st;
     size_t blk0, off0;
     std::unique_lock<std::recursive_mutex> lock;
     Scratch(heb_ctx *c, cudaStream_t st);
     cudaError_t get(size_t bytes) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) a->captured = true;
         bytes = (bytes + 255) & ~(size_t)255;
         if (!bytes) bytes = 256;
         while (a->blk < a->blocks.size()) {
@@ -148,7 +154,7 @@ struct Scratch {
         a->off = off0;
     }
 };
-inline Scratch::Scratch(heb_ctx *c, cudaStream_t st) : a(c->arena(st)), lock(a->mu) {
+inline Scratch::Scratch(heb_ctx *c, cudaStream_t st_) : a(c->arena(st_)), st(st_), lock(a->mu) {
     blk0 = a->blk;
     off0 = a->off;
 }

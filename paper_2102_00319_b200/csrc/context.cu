@@ -238,9 +238,24 @@ extern "C" int heb_ctx_release_scratch(heb_ctx *c, void *stream) {
     }
     std::lock_guard<std::recursive_mutex> g(a->mu);
     if (a->blk != 0 || a->off != 0) return fail(HEB_EINVAL, "heb_ctx_release_scratch: scratch in use");
+    if (a->captured)
+        return fail(HEB_EINVAL,
+                    "heb_ctx_release_scratch: CUDA graphs captured on this stream use its scratch "
+                    "(destroy them, then heb_ctx_clear_captured)");
     CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));  // queued work may still read it
     for (auto &b : a->blocks) cudaFree(b.base);
     a->blocks.clear();
+    return HEB_OK;
+}
+
+extern "C" int heb_ctx_clear_captured(heb_ctx *c, void *stream) {
+    if (!c) return fail(HEB_EINVAL, "heb_ctx_clear_captured: null context");
+    std::lock_guard<std::mutex> g(c->arena_mu);
+    auto it = c->arenas.find((cudaStream_t)stream);
+    if (it != c->arenas.end()) {
+        std::lock_guard<std::recursive_mutex> ga(it->second->mu);
+        it->second->captured = false;
+    }
     return HEB_OK;
 }
 

@@ -357,11 +357,14 @@ class LayerEvaluator:
         self.be.counters.bump(ctct_add=dout)
         return CipherBatch(out, min(y.level, bias.level), scale, noise_sum(noise, bias.noise_bits))
 
-    def run(self, enc: EncryptedNetworkBatch, x: CipherBatch) -> CipherBatch:
+    def run(self, enc: EncryptedNetworkBatch, x: CipherBatch, deltas: list | None = None) -> CipherBatch:
+        """One inference over the batch; ``deltas`` (optional) receives (layer kind, counter
+        delta) per layer, the runtime side of ``analyzer.verify_against_runtime``."""
         net = enc.net
         dims = (1, *net.input_dims)
         flat_map = None
         for li, layer in enumerate(net.layers):
+            before = self.be.counters.snapshot() if deltas is not None else None
             if isinstance(layer, Conv):
                 x, dims = self.conv(x, dims, layer, enc.weights[li], enc.biases[li])
             elif isinstance(layer, Square):
@@ -376,6 +379,8 @@ class LayerEvaluator:
                 flat_map = (c * (m * n) + i * n + j).ravel()  # flat[(i*n+j)*C + c] = map[c][i][j]
             elif isinstance(layer, Dense):
                 x = self.dense(x, flat_map, layer, enc.weights[li], enc.biases[li])
+            if deltas is not None:
+                deltas.append((layer.kind, self.be.counters.snapshot() - before))
         return x
 
 
@@ -420,6 +425,14 @@ class LayerEvaluator:
             graph.instantiate()
             hit = self._graphs[key] = (graph, out, delta, enc, x.buf)  # keep the captured buffers alive
         return hit[:3]
+
+    def drop_graphs(self) -> None:
+        """Destroy every captured graph; their streams' scratch may then be released."""
+        streams = {self._pipeline_streams("compute", key[-1] + 1)[key[-1]] for key in self._graphs}
+        self._graphs.clear()
+        torch.cuda.synchronize(self.be.dev)
+        for st in streams:
+            self.ctx.call("heb_ctx_clear_captured", st.cuda_stream)
 
     def graph_kernel_launches(self, enc: EncryptedNetworkBatch, x: CipherBatch, pipeline: int = 0) -> int:
         """Kernel nodes of the captured CUDA graph of one inference (= kernel launches per

@@ -103,11 +103,13 @@ def poly_act_cell(backend, y, pt_quad, pt_lin, pt_const):
     return backend.add_ct_pt(backend.add_ct_ct(quad, lin), pt_const)
 
 
-def run_network(backend, enc: EncryptedNetwork, maps: list) -> list:
-    """Evaluate the encrypted network op by op; returns the logit ciphertexts."""
+def run_network(backend, enc: EncryptedNetwork, maps: list, deltas: list | None = None) -> list:
+    """Evaluate the encrypted network op by op; returns the logit ciphertexts.
+    ``deltas`` (optional) receives (layer kind, counter delta) per layer."""
     net = enc.net
     flat = None
     for li, layer in enumerate(net.layers):
+        before = backend.counters.snapshot() if deltas is not None else None
         if isinstance(layer, Conv):
             w = enc.weights[li]
             p, q = layer.kernel
@@ -175,4 +177,6 @@ def run_network(backend, enc: EncryptedNetwork, maps: list) -> list:
                     cell = backend.add_ct_ct(cell, enc.biases[li][r])
                 out.append(cell)
             flat = out
+        if deltas is not None:
+            deltas.append((layer.kind, backend.counters.snapshot() - before))
     return flat
