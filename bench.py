@@ -380,6 +380,115 @@ def run_gpu(args) -> None:
         dist.destroy_process_group()
 
 
+def run_cfg5(args) -> None:
+    """BASELINE config 5: the config-4 network on 4 independent seeded 16384-image
+    batches (same keys and weights), sharded over WORLD_SIZE GPUs (strong scaling: the
+    total work is fixed).  Ranks take whole batches while world <= 4; beyond that each
+    batch is split into world / 4 bands of conv2 output rows (conv1 / x^2 halo recomputed,
+    sharding.run_band_shard) whose FC raw partials are all-gathered within the batch's
+    rank group over NCCL -- the path's one real exchange -- summed mod p and finalised.
+    value = 4 batches x 16384 images / max-over-ranks device time per step."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2102_00319_b200 import layers
+    from paper_2102_00319_b200 import sharding as sh
+    from paper_2102_00319_b200.backend import B200Backend
+    from paper_2102_00319_b200.configs import BATCH, CONFIGS, IMAGE_SEEDS, NETWORKS, cnn_images
+    from paper_2102_00319_b200.model import plaintext_forward
+
+    batches = 4
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = CONFIGS["cfg4"]
+    be = B200Backend(cfg.params(), cfg.base_extra_bits, device=local)
+    keys = be.keygen()
+    be.set_eval_key(keys)
+    net = NETWORKS["cfg4"]()
+    enc = layers.encrypt_network(be, net, keys)
+    batch = min(BATCH["cfg4"], be.slots)
+    plan = sh.plan_batches(batches, world)[rank]
+    per = max(1, world // batches)
+    lay = sh.BandLayout.of(net)
+    bands = sh.plan_bands(lay.rows2, per)
+    images = {b: cnn_images(batch, IMAGE_SEEDS["cfg4"] + b) for b, _ in plan}
+    xs = {b: layers.encrypt_images(be, images[b], keys) for b, _ in plan}
+    ev = layers.LayerEvaluator(be)
+    stream = torch.cuda.current_stream()
+    group = None
+    if per > 1:
+        groups = [dist.new_group(list(range(g * per, (g + 1) * per))) for g in range(world // per)]
+        group = groups[rank // per]
+
+    def step():
+        outs = {}
+        for b, band in plan:
+            if per == 1:
+                outs[b] = ev.run(enc, xs[b])
+                continue
+            raw, lvl, scale, noise = ev.run_band_shard(enc, xs[b], bands[band])
+            got = [torch.empty_like(raw) for _ in range(per)]
+            dist.all_gather(got, raw, group=group)
+            if band == 0:
+                outs[b] = ev.finish_cells(enc, torch.stack(got), lvl, scale, noise)
+        return outs
+
+    out = step()  # correctness check: decrypted logits vs the float64 plaintext forward pass
+    err, argmax_ok = 0.0, True
+    for b, y in out.items():
+        dec = be.decrypt_batch(y, keys)[:, :batch].T
+        ref = plaintext_forward(net, images[b][:64])
+        err = max(err, float(np.max(np.abs(dec[:64] - ref))))
+        argmax_ok = argmax_ok and bool(np.array_equal(np.argmax(dec[:64], 1), np.argmax(ref, 1)))
+    del out
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    clocks.mark()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = torch.tensor([t0.elapsed_time(t1)], device="cuda")
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_max = float(ms.item())
+    value = batches * batch * args.steps / (ms_max / 1e3)
+    if rank == 0:
+        peaks = load_peaks()
+        path_rate = PATH_BYTES_PER_BATCH["cfg4"] * value / batch / 1e9
+        print(json.dumps({
+            "metric": BASELINE_METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (4 seeded U[0,1] 28x28 image batches, N(0,0.05^2) weights; MNIST absent)",
+            "config": {"workload": f"cfg5: the cfg4 network on {batches} batches of {batch} images, N={be.n}",
+                       "batches": batches, "batch": batch, "parallelism": (
+                           f"{world} ranks: whole batches" if per == 1 else
+                           f"{world} ranks: {per} conv2-row bands per batch (halo recompute), FC partials "
+                           f"all-gathered per batch over NCCL"),
+                       "l2_policy": "inputs larger than L2"},
+            "path_roofline": {"achieved_gbs": round(path_rate, 2), "frac_of_hbm": round(path_rate / peaks["hbm_gbs"], 4),
+                              "source": "SURVEY.md §8(d) cfg4 layer-wise compulsory bytes"},
+            "clocks": clk,
+            "check": {"max_abs_err_vs_plaintext": err, "argmax_identical": argmax_ok, "images_checked": 64},
+        }), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def cfg1_ops(args, device: int) -> dict:
     """Config 1 primitive ops/s on the device: 256 seeded pairs per batched call, calls
     issued round-robin on the bench's pipeline count of concurrent streams.  Ops (SURVEY
@@ -804,8 +913,9 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="cfg4", choices=["cfg2", "cfg3", "cfg4"],
-                    help="BASELINE config; cfg4 (N = 32768, the largest single-GPU config) is the headline")
+    ap.add_argument("--config", default="cfg4", choices=["cfg2", "cfg3", "cfg4", "cfg5"],
+                    help="BASELINE config; cfg4 (N = 32768, the largest single-GPU config) is the headline; "
+                         "cfg5 = the cfg4 network on 4 batches sharded over the ranks (strong scaling)")
     ap.add_argument("--pipelines", type=int, default=None,
                     help="concurrent inference pipelines (streams) per GPU (default: per config)")
     ap.add_argument("--no-prof", action="store_true", help="no per-kernel events in the timed region")
@@ -814,9 +924,13 @@ def main() -> None:
     ap.add_argument("--skip-u64", action="store_true", help="no e2e run in the reference's u64 payload format")
     args = ap.parse_args()
     if args.pipelines is None:
-        args.pipelines = PIPELINES[args.config]
+        args.pipelines = PIPELINES.get(args.config, 1)
     if args.impl == "reference":
+        if args.config == "cfg5":
+            args.config = "cfg4"  # the reference arm times the same network per batch
         run_reference(args)
+    elif args.config == "cfg5":
+        run_cfg5(args)
     else:
         run_gpu(args)
 

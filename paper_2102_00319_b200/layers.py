@@ -615,6 +615,56 @@ class LayerEvaluator:
         fidx = self._idx(("shard_fc", key), build_fc)
         return self.dot(pooled_b, enc.weights[4], fidx[0], fidx[1], len(pooled), dout)
 
+    # -- bands-mode sharding (sharding.py): a two-conv network's batch split by conv2 rows --
+    def run_band_shard(self, enc: EncryptedNetworkBatch, x: CipherBatch, band: tuple[int, int]) -> tuple:
+        """This rank's FC raw partials (out_dim, 3, k, N) over conv2 output rows [a, b):
+        conv1 + act over the rows the band reads (halo recomputed), conv2 + act over the
+        band, the band's cells of every pool window it touches summed in WINDOW_ORDER
+        (a window cut by the band boundary is summed partially), FC partial sums over the
+        window sums.  Returns (raw, level, scale, noise) like ``dot``."""
+        from . import sharding as sh
+
+        net = enc.net
+        lay = sh.BandLayout.of(net)
+        a, b = band
+        c1, act1, c2, act2, dense = (net.layers[i] for i in (0, 1, 2, 3, 6))
+        if c1.channels != 1:
+            raise ValueError("band sharding reads input rows of a single-channel image grid")
+        i0, i1 = lay.input_rows(a, b)
+        n_in = lay.in_cols
+        xb = CipherBatch(x.buf[i0 * n_in: i1 * n_in], x.level, x.scale, x.noise_bits)  # a contiguous row band
+        y, dims = self.conv(xb, (1, i1 - i0, n_in), c1, enc.weights[0], enc.biases[0])
+        y = self.square(y) if isinstance(act1, Square) else self.poly_act(y, act1)
+        y, (F2, rb, cols) = self.conv(y, dims, c2, enc.weights[2], enc.biases[2])
+        y = self.square(y) if isinstance(act2, Square) else self.poly_act(y, act2)
+        # full windows first, then the windows cut by a band boundary (2 of their 4 cells)
+        wins = sorted(lay.windows(a, b), key=lambda w: -len(w[3]))
+        pooled = self._empty(len(wins), 2, y.k)
+        off = 0
+        for terms in (4, 2):
+            sel = [w for w in wins if len(w[3]) == terms]
+            if not sel:
+                continue
+            pidx = self._idx(("band_pool", band, terms), lambda: np.array(
+                [[f * rb * cols + (i - a) * cols + jj for i, jj in cells] for f, _, _, cells in sel]))
+            self.ctx.call("heb_sum_gather", y.desc(), pidx.data_ptr(), terms, ct_desc(pooled[off: off + len(sel)]),
+                          len(sel), 2, y.k, self.ctx.stream)
+            self.be.counters.bump(ctct_add=(terms - 1) * len(sel))
+            off += len(sel)
+        pnoise = y.noise_bits
+        for _ in range(3):
+            pnoise = noise_sum(pnoise, y.noise_bits)
+        dout = dense.out_dim
+
+        def build_fc():
+            ia = np.broadcast_to(np.arange(len(wins))[None, :], (dout, len(wins)))
+            flat = np.array([lay.flat_of(f, r, j) for f, r, j, _ in wins])
+            return np.stack([ia, flat[None, :] * dout + np.arange(dout)[:, None]])
+
+        fidx = self._idx(("band_fc", band), build_fc)
+        return self.dot(CipherBatch(pooled, y.level, y.scale, pnoise), enc.weights[6], fidx[0], fidx[1], len(wins),
+                        dout)
+
     def finish_cells(self, enc: EncryptedNetworkBatch, parts: torch.Tensor, level: int, scale: Fraction,
                      noise: float) -> CipherBatch:
         """Add the gathered partials (world, out, 3, k, N) mod p, relinearise + rescale, bias."""
@@ -626,7 +676,7 @@ class LayerEvaluator:
         self.ctx.call("heb_sum_gather", ct_desc(flat), idx.data_ptr(), world, ct_desc(raw), dout, 3, k, self.ctx.stream)
         self.be.counters.bump(ctct_add=dout * (world - 1))
         y = self.finalize(raw, level, scale, noise + math.log2(world))
-        bias = enc.biases[4]
+        bias = enc.biases[len(enc.net.layers) - 1]  # the dense layer is last
         return self.add(y, bias) if bias is not None else y
 
 

@@ -14,6 +14,16 @@ data-path exchange except the final logits:
   added mod p -- exact, so the result is bit-identical to one device
   (`base.py:144-153`) -- and finalised once (`dense_combine`, `layers.py:262-272`).
 
+* ``bands`` mode -- for two-convolution networks (config 4 / config 5: conv1 -> act ->
+  conv2 -> act -> pool -> flatten -> dense) one batch is split over ranks by contiguous
+  bands of conv2 output rows (the reference's horizontal band split with a (P-1)-row
+  overlap, `executor.py:86-112`): each rank recomputes the conv1 / act rows
+  its band reads (the halo) and its conv2 / act cells, sums its cells of every pool window
+  it touches (a window cut by a band boundary is summed partially on both ranks), and
+  forms the FC layer's degree-2 partial sums over those window sums.  Tensor products are
+  bilinear and raw additions exact mod p, so the gathered, summed partials equal the
+  single-device accumulation bit for bit.
+
 The collectives are plain ``torch.distributed`` calls on int64-typed tensors
 (NCCL over NVLink on B200 ranks, gloo in the CPU tests); the modular sum of the
 gathered partials runs on the device (``heb_sum_gather``) or through the backend's
@@ -126,6 +136,139 @@ def percell_fc_partials(backend, enc, grid, units) -> list:
         acc = None
         for key in order:
             t = backend.mul_ct_ct_raw(pooled[key], dw[flat_of(lay, *key), cls])
+            acc = t if acc is None else backend.raw_add(acc, t)
+        parts.append(acc)
+    return parts
+
+
+@dataclass(frozen=True)
+class BandLayout:
+    """Shape facts of a conv -> act -> conv -> act -> sumpool -> flatten -> dense network."""
+
+    in_rows: int
+    in_cols: int
+    s1: int            # conv1 stride
+    p1: int            # conv1 kernel rows
+    rows1: int         # conv1 output rows
+    cols1: int
+    p2: int            # conv2 kernel rows (stride 1)
+    rows2: int         # conv2 output rows
+    cols2: int
+    filters2: int
+    pool_cols: int
+
+    @classmethod
+    def of(cls, net: Network) -> "BandLayout":
+        kinds = [l.kind for l in net.layers]
+        if len(kinds) != 7 or kinds[0] != "conv" or kinds[2] != "conv" or kinds[4] != "sumpool" \
+                or kinds[5] != "flatten" or kinds[6] != "dense" or kinds[1] not in ("square", "polyact") \
+                or kinds[3] not in ("square", "polyact"):
+            raise ValueError("band sharding needs conv -> act -> conv -> act -> sumpool -> flatten -> dense")
+        c1, c2 = net.layers[0], net.layers[2]
+        if c2.stride != 1:
+            raise ValueError("band sharding needs a stride-1 second convolution")
+        m, n = net.input_dims
+        r1, k1 = c1.out_dims(m, n)
+        r2, k2 = c2.out_dims(r1, k1)
+        return cls(m, n, c1.stride, c1.kernel[0], r1, k1, c2.kernel[0], r2, k2, c2.filters, k2 // 2)
+
+    def conv1_rows(self, a: int, b: int) -> tuple[int, int]:
+        """conv1 output rows [a, b + p2 - 1) feed conv2 rows [a, b) (the halo)."""
+        return a, b + self.p2 - 1
+
+    def input_rows(self, a: int, b: int) -> tuple[int, int]:
+        r0, r1 = self.conv1_rows(a, b)
+        return r0 * self.s1, (r1 - 1) * self.s1 + self.p1
+
+    def windows(self, a: int, b: int) -> list[tuple[int, int, int, list[tuple[int, int]]]]:
+        """Pool windows (f, r, j) touched by conv2 rows [a, b), each with the conv2 cells
+        (row, col) of the window this band owns, in WINDOW_ORDER."""
+        out = []
+        for f in range(self.filters2):
+            for r in range(a // 2, (b + 1) // 2):
+                for j in range(self.pool_cols):
+                    cells = [(2 * r + di, 2 * j + dj) for di, dj in WINDOW_ORDER if a <= 2 * r + di < b]
+                    if cells:
+                        out.append((f, r, j, cells))
+        return out
+
+    def flat_of(self, f: int, r: int, j: int) -> int:
+        return (r * self.pool_cols + j) * self.filters2 + f
+
+
+def plan_bands(rows: int, parts: int) -> list[tuple[int, int]]:
+    """``parts`` contiguous, balanced bands of conv2 output rows."""
+    if parts < 1 or parts > rows:
+        raise ValueError(f"cannot split {rows} rows into {parts} bands")
+    return [((rows * i) // parts, (rows * (i + 1)) // parts) for i in range(parts)]
+
+
+def plan_batches(batches: int, world: int) -> list[list[tuple[int, int]]]:
+    """Config 5: ``batches`` independent batches over ``world`` ranks.  Returns per rank a
+    list of (batch, band index) work items together with the band count per batch: ranks
+    take whole batches while world <= batches, and split each batch into world / batches
+    bands beyond that."""
+    if world <= batches:
+        if batches % world:
+            raise ValueError("world must divide the batch count")
+        return [[(b, 0) for b in range(r, batches, world)] for r in range(world)]
+    if world % batches:
+        raise ValueError("batch count must divide the world")
+    per = world // batches
+    return [[(r // per, r % per)] for r in range(world)]
+
+
+def percell_band_partials(backend, enc, grid, band: tuple[int, int]) -> list:
+    """This band's FC raw partial per class, composed from public HEBackend ops only."""
+    from .percell import act_plaintexts, poly_act_cell
+
+    net = enc.net
+    lay = BandLayout.of(net)
+    a, b = band
+    c1, act1, c2, act2, dense = net.layers[0], net.layers[1], net.layers[2], net.layers[3], net.layers[6]
+
+    def act(layer, cells):
+        if isinstance(layer, Square):
+            return {k: backend.mul_ct_ct(v, v) for k, v in cells.items()}
+        first = next(iter(cells.values()))
+        pts = act_plaintexts(backend, layer, first.level, first.scale)
+        return {k: poly_act_cell(backend, v, *pts) for k, v in cells.items()}
+
+    def conv(layer, w, bias, src, rows, cols):
+        p, q = layer.kernel
+        s = layer.stride
+        out = {}
+        for f in range(layer.filters):
+            for i in range(*rows):
+                for j in range(cols):
+                    acc = None
+                    for c in range(layer.channels):
+                        for dp in range(p):
+                            for dq in range(q):
+                                t = backend.mul_ct_ct_raw(src(c, i * s + dp, j * s + dq), w[f, c, dp, dq])
+                                acc = t if acc is None else backend.raw_add(acc, t)
+                    y = backend.raw_finalize(acc)
+                    if bias is not None:
+                        y = backend.add_ct_ct(y, bias[f])
+                    out[(f, i, j)] = y
+        return out
+
+    y1 = act(act1, conv(c1, enc.weights[0], enc.biases[0], lambda c, i, j: grid[c][i][j], lay.conv1_rows(a, b),
+                        lay.cols1))
+    y2 = act(act2, conv(c2, enc.weights[2], enc.biases[2], lambda c, i, j: y1[(c, i, j)], (a, b), lay.cols2))
+    sums = {}
+    for f, r, j, cells in lay.windows(a, b):
+        acc = None
+        for i, jj in cells:
+            acc = y2[(f, i, jj)] if acc is None else backend.add_ct_ct(acc, y2[(f, i, jj)])
+        sums[(f, r, j)] = acc
+    order = sorted(sums, key=lambda k: lay.flat_of(*k))
+    dw = enc.weights[6]
+    parts = []
+    for cls in range(dense.out_dim):
+        acc = None
+        for key in order:
+            t = backend.mul_ct_ct_raw(sums[key], dw[lay.flat_of(*key), cls])
             acc = t if acc is None else backend.raw_add(acc, t)
         parts.append(acc)
     return parts
