@@ -138,6 +138,16 @@ class DevCipher:
     def rows(self) -> "torch.Tensor":
         return self.buf[:, : self.k]
 
+    # host copies in the reference CkksCipher layout ((k, N) uint64 per component), for
+    # callers that inspect payload residues (reference tests, debugging)
+    @property
+    def c0(self) -> np.ndarray:
+        return dev_to_u64(self.buf[0, : self.k])
+
+    @property
+    def c1(self) -> np.ndarray:
+        return dev_to_u64(self.buf[1, : self.k])
+
 
 @dataclass(frozen=True)
 class DevRaw:

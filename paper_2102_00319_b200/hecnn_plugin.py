@@ -56,12 +56,25 @@ def make_backend_class():
             self.ctx = dev.ctx
 
         # -- keys ------------------------------------------------------------------
+        # The reference's key payloads are numpy arrays (CkksSecret.s_eval, CkksPublic.b/a);
+        # the device keys stay on the device and are exposed through host views of the
+        # same names, so callers that inspect key residues see the reference layout.
         def _wrap_key(self, k):
-            return hb.KeyMaterial(fingerprint=self.fingerprint, backend_name=self.name, public=k.public,
-                                  secret=k.secret, evaluation=k.evaluation)
+            return hb.KeyMaterial(fingerprint=self.fingerprint, backend_name=self.name,
+                                  public=None if k.public is None else _HostPublic(k.public),
+                                  secret=None if k.secret is None else _HostSecret(k.secret),
+                                  evaluation=k.evaluation)
+
+        @staticmethod
+        def _device_key(key):
+            return _DevKey(public=getattr(key.public, "dev", key.public), secret=getattr(key.secret, "dev", key.secret),
+                           evaluation=key.evaluation)
 
         def keygen(self):
             return self._wrap_key(self._dev.keygen())
+
+        def _fresh_noise_bits(self) -> float:  # CkksBackend._fresh_noise_bits (ckks.py:231-235)
+            return self._dev._fresh_noise_bits()
 
         def set_eval_key(self, key) -> None:
             super().set_eval_key(key)
@@ -72,10 +85,10 @@ def make_backend_class():
             return self._dev._encode_impl(values, scale, level)
 
         def _encrypt_impl(self, values, scale, key, entropy):
-            return self._dev._encrypt_impl(values, scale, key, entropy)
+            return self._dev._encrypt_impl(values, scale, self._device_key(key), entropy)
 
         def _decrypt_impl(self, ct, key):
-            return self._dev._decrypt_impl(ct, key)
+            return self._dev._decrypt_impl(ct, self._device_key(key))
 
         def _drop_impl(self, ct, level):
             return self._dev._drop_impl(ct, level)
@@ -109,7 +122,7 @@ def make_backend_class():
                                 fingerprint=self.fingerprint, backend_name=self.name, noise_bits=noise_bits)
 
         def key_payload_bytes(self, key) -> dict[str, bytes]:
-            return self._dev.key_payload_bytes(key)
+            return self._dev.key_payload_bytes(self._device_key(key))
 
         def key_from_payload(self, parts: dict[str, bytes]):
             return self._wrap_key(self._dev.key_from_payload(parts))
@@ -119,6 +132,45 @@ def make_backend_class():
             return self._dev.cipher_rows_host(ct)
 
     return HecnnB200Backend
+
+
+class _HostSecret:
+    """Device secret key with a host view ``s_eval`` (reference CkksSecret layout)."""
+
+    def __init__(self, dev):
+        self.dev = dev
+
+    @property
+    def s_eval(self):
+        from .backend import dev_to_u64
+
+        return dev_to_u64(self.dev.s_eval)
+
+
+class _HostPublic:
+    """Device public key with host views ``b`` / ``a`` (reference CkksPublic layout)."""
+
+    def __init__(self, dev):
+        self.dev = dev
+
+    @property
+    def b(self):
+        from .backend import dev_to_u64
+
+        return dev_to_u64(self.dev.b)
+
+    @property
+    def a(self):
+        from .backend import dev_to_u64
+
+        return dev_to_u64(self.dev.a)
+
+
+class _DevKey:
+    """The device parts of a key bundle, for the device hooks."""
+
+    def __init__(self, public, secret, evaluation):
+        self.public, self.secret, self.evaluation = public, secret, evaluation
 
 
 _CLASS = None

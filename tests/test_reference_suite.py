@@ -32,7 +32,8 @@ INTERNAL = {
     "test_pipeline_invariants.py::test_decrypt_detects_out_of_range_coefficients",
 }
 
-SUITES = ["test_backend_contract.py", "test_backend_agreement.py", "test_executor.py", "test_pipeline_invariants.py"]
+SUITES = ["test_backend_contract.py", "test_backend_agreement.py", "test_executor.py", "test_pipeline_invariants.py",
+          "test_layers.py", "test_model.py", "test_packing.py"]
 
 
 def hecnn_importable() -> bool:
@@ -58,14 +59,14 @@ def test_plugin_is_a_reference_backend():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("suite", SUITES)
-def test_reference_suite_on_device_backend(suite, tmp_path):
+def test_reference_suite_on_device_backend(suite):
     if not os.path.exists(os.path.join(REF_TESTS, suite)) or not hecnn_importable():
         pytest.skip("reference suite not installed (tools/install_reference.sh)")
     env = dict(os.environ, PYTHONPATH=f"{REF}:{REPO}:{REF_TESTS}", HECNN_CKKS_IMPL="b200")
-    deselect = [a for t in INTERNAL if t.startswith(suite) for a in ("--deselect", os.path.join(REF_TESTS, t))]
-    res = subprocess.run([sys.executable, "-m", "pytest", os.path.join(REF_TESTS, suite), "-q", "-p",
-                          "paper_2102_00319_b200.hecnn_plugin", "-p", "no:cacheprovider", "-rf", *deselect],
-                         env=env, capture_output=True, text=True, cwd=str(tmp_path), timeout=1500)
+    deselect = [a for t in INTERNAL if t.startswith(suite) for a in ("--deselect", t)]
+    res = subprocess.run([sys.executable, "-m", "pytest", suite, "-q", "-p", "paper_2102_00319_b200.hecnn_plugin",
+                          "-p", "no:cacheprovider", "-rf", *deselect],
+                         env=env, capture_output=True, text=True, cwd=REF_TESTS, timeout=1500)
     tail = res.stdout[-4000:]
     summary = re.findall(r"(\d+) (passed|failed|error)", tail)
     counts = {k: int(v) for v, k in summary}
