@@ -298,6 +298,7 @@ def run_gpu(args) -> None:
 
     # ---- int64 modmul peak (microbenchmark) ---------------------------------------------
     peak_mm = modmul_peak(be) if rank == 0 else None
+    peak_bf = butterfly_peaks(be) if rank == 0 else None
 
     if rank == 0:
         peaks = load_peaks()
@@ -357,6 +358,7 @@ def run_gpu(args) -> None:
                         "so the integer Shoup peak is not an upper bound for the mix",
             },
             "compute_roofline": ncu_pipes(name, args.config),
+            "butterfly_roofline": butterfly_roofline(net, be, x.level, prof, args.steps, peak_bf),
             "kernels": {k: {"launches": v[0], "ms": round(v[1], 3), "gbs": round(v[2] / max(v[1], 1e-9) / 1e6, 1)}
                         for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
             "cpu_baseline": cpu,
@@ -587,9 +589,97 @@ def modmul_peak(be) -> float:
     return blocks * threads * iters * 8 / (ms.value / 1e3)
 
 
+def butterfly_peaks(be) -> dict:
+    """Measured register-only butterfly ceilings of the two NTT engines (heb_bench_butterfly)."""
+    import ctypes
+
+    import torch
+
+    from paper_2102_00319_b200 import _lib
+
+    primes = [int(q) for q in be.chain.primes]
+    small = [q for q in primes if q < (1 << 42)]
+    wide = [q for q in primes if q >= (1 << 42)] or primes
+    out = {}
+    blocks, threads, iters = 148 * 8, 256, 512
+    for kind, name, q in ((1, "fp64", small[0] if small else None), (2, "int", wide[0])):
+        if q is None:
+            continue
+        ms = ctypes.c_double()
+        _lib.call("heb_bench_butterfly", kind, blocks, threads, iters, q, ctypes.byref(ms),
+                  torch.cuda.current_stream().cuda_stream)
+        out[name] = blocks * threads * iters * 128 / (ms.value / 1e3)
+    return out
+
+
+def modup_butterflies(net, be, top_level: int) -> dict:
+    """Butterflies and key products of the fused ModUp launches of one inference, from the network
+    shape: a relinearisation of `items` ciphertexts at k rows runs, for every target row t (the k
+    chain rows and the special prime), one N-point transform per digit j != t ((N/2) log N
+    butterflies each) and 2 N key products per digit."""
+    from paper_2102_00319_b200.analyzer import analyze
+
+    n = be.n
+    logn = n.bit_length() - 1
+    primes = [int(q) for q in be.chain.primes]  # chain rows, then the special prime
+    is_fp = [q < (1 << 42) for q in primes[:-1]]  # engine of each chain row (ntt.cuh: FP64 engine below 2^42)
+    special_fp = primes[-1] < (1 << 42)
+    rep = analyze(net, be.params)
+    level = top_level
+    fp = integer = keyprod = 0
+    relins = []
+    for lc in rep.per_layer:
+        if lc.name in ("conv", "square", "polyact", "dense"):
+            k = level + 1
+            per_t = (n // 2) * logn
+            t_fp = sum((k - 1) for t in range(k) if is_fp[t]) + (k if special_fp else 0)
+            t_int = sum((k - 1) for t in range(k) if not is_fp[t]) + (0 if special_fp else k)
+            fp += lc.out_cts * t_fp * per_t
+            integer += lc.out_cts * t_int * per_t
+            keyprod += lc.out_cts * (k + 1) * k * 2 * n
+            relins.append({"layer": lc.name, "items": lc.out_cts, "rows": k})
+        level -= lc.levels
+    return {"fp64": fp, "int": integer, "key_products": keyprod, "relinearisations": relins}
+
+
 def ncu_record_path(config: str) -> str:
     """The committed ncu --set full capture of this config's top kernel."""
     return os.path.join(REPO, "profiles", f"ncu_top_kernel_{config}.json")
+
+
+def butterfly_roofline(net, be, top_level, prof, steps, peaks):
+    """Compute roofline of the fused ModUp: its NTT butterflies per second against the measured
+    register-only butterfly ceilings of the two engines, weighted by the row mix.  The two engine
+    launches run concurrently (DFMA vs IMAD/ALU pipes), so the ceiling is the slower engine's time
+    (`ceiling_overlapped`); `ceiling_serial` adds the two times.  Key products ride on top of the
+    butterflies (not counted in `achieved`), so `frac` understates the pipe use."""
+    rec = prof.get("k_ks_modup_fused")
+    if not rec or not peaks or "int" not in peaks:
+        return None
+    w = modup_butterflies(net, be, top_level)
+    ms = rec[1] / steps
+    t_fp = w["fp64"] / peaks["fp64"] if "fp64" in peaks and w["fp64"] else 0.0
+    t_int = w["int"] / peaks["int"]
+    total = w["fp64"] + w["int"]
+    achieved = total / (ms / 1e3)
+    over = total / max(t_fp, t_int)
+    serial = total / (t_fp + t_int)
+    return {
+        "kernel": "k_ks_modup_fused",
+        "butterflies_per_step": {"fp64_engine": w["fp64"], "int_engine": w["int"]},
+        "key_products_per_step": w["key_products"],
+        "ms_per_step": round(ms, 3),
+        "achieved_gbf_s": round(achieved / 1e9, 1),
+        "peak_fp64_gbf_s": round(peaks.get("fp64", 0.0) / 1e9, 1),
+        "peak_int_gbf_s": round(peaks["int"] / 1e9, 1),
+        "ceiling_overlapped_gbf_s": round(over / 1e9, 1),
+        "ceiling_serial_gbf_s": round(serial / 1e9, 1),
+        "frac": round(achieved / over, 4),
+        "frac_serial": round(achieved / serial, 4),
+        "relinearisations": w["relinearisations"],
+        "measured": "heb_bench_butterfly (registers only, the engines' own butterfly code) in this run; "
+                    "ModUp time from the per-kernel event pass",
+    }
 
 
 def ncu_traffic(kernel: str, config: str):

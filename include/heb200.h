@@ -234,6 +234,10 @@ int heb_prof_summary(char *buf, size_t len);
 int heb_prof_next_bytes(double bytes);
 /* Shoup 64-bit modmul throughput microbenchmark (blocks*threads*iters*8 modmuls). */
 int heb_bench_modmul(int blocks, int threads, int iters, uint64_t p, double *ms_out, void *stream);
+/* NTT butterfly throughput microbenchmark, registers only (blocks*threads*iters*128 butterflies):
+ * kind 1 = FP64 engine (p < 2^42), kind 2 = integer Shoup engine.  The measured ceilings of
+ * the transform kernels' compute roofline (bench.py `butterfly_roofline`). */
+int heb_bench_butterfly(int kind, int blocks, int threads, int iters, uint64_t p, double *ms_out, void *stream);
 
 #ifdef __cplusplus
 }

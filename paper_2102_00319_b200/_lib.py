@@ -82,6 +82,7 @@ SIGNATURES: dict[str, list] = {
     "heb_prof_summary": [ctypes.c_char_p, ctypes.c_size_t],
     "heb_prof_next_bytes": [ctypes.c_double],
     "heb_bench_modmul": [_I, _I, _I, _U, ctypes.POINTER(ctypes.c_double), _P],
+    "heb_bench_butterfly": [_I, _I, _I, _I, _U, ctypes.POINTER(ctypes.c_double), _P],
 }
 _RET = {"heb_last_error": ctypes.c_char_p, "heb_version": ctypes.c_int, "heb_ctx_ring_degree": ctypes.c_int,
         "heb_packed_words": ctypes.c_int64}

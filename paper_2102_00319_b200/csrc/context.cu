@@ -428,3 +428,91 @@ extern "C" int heb_bench_modmul(int blocks, int threads, int iters, uint64_t p, 
     CUDA_TRY(cudaFreeAsync(sink, st));
     return HEB_OK;
 }
+
+// =============================================================================
+// NTT butterfly microbenchmark: the compute-roofline denominators of the transform
+// kernels.  Each thread keeps one radix-16 unit (16 residues) in registers and runs
+// `iters` transform-equivalents of 4 register groups (4 levels x 8 butterflies each, the
+// engines' own ar.fwd) with twiddles in registers and no memory traffic; the FP64 engine
+// re-centres once per transform-equivalent like a real transform's output does.
+//   kind 1: FP64 engine (p < 2^42, DFMA pipe)   kind 2: integer Shoup engine (IMAD / ALU)
+// =============================================================================
+template <class A>
+__device__ __forceinline__ void bench_unit(const A &ar, typename A::V (&x)[16], const typename A::W (&w)[4]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int half = 8 >> q;
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            if (m & half) continue;
+            ar.fwd(x[m], x[m + half], w[q]);
+        }
+    }
+}
+__global__ void __launch_bounds__(256) k_bench_bfly_fp(double *sink, double p, double pinv, int iters) {
+    const ntt::FpArith ar(p, pinv);
+    double x[16], w[4];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = (double)((threadIdx.x * 16 + i) * 2654435761u % 1000003u);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[q] = floor(p * (0.31 + 0.17 * q));
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) bench_unit(ar, x, w);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[i] = ntt::fred(x[i], p, pinv);
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += x[i];
+    if (s == 0.123456789) sink[0] = s;
+}
+__global__ void __launch_bounds__(256) k_bench_bfly_int(u64 *sink, u64 p, int iters) {
+    const ntt::IntArith ar(p);
+    u64 x[16];
+    ulonglong2 w[4];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = ((u64)(threadIdx.x * 16 + i) * 0x9e3779b97f4a7c15ull) % p;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const u64 v = (p >> 1) + 12345 + 77 * q;
+        w[q] = make_ulonglong2(v, (u64)(((u128)v << 64) / p));
+    }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) bench_unit(ar, x, w);
+    }
+    u64 s = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s ^= x[i];
+    if (s == 0x9e3779b97f4a7c15ull) sink[0] = s;
+}
+
+// blocks x threads threads, each iters x 128 butterflies; elapsed ms out.
+extern "C" int heb_bench_butterfly(int kind, int blocks, int threads, int iters, uint64_t p, double *ms_out,
+                                   void *stream) {
+    if ((kind != 1 && kind != 2) || blocks < 1 || threads < 32 || threads > 256 || iters < 1 || !ms_out)
+        return fail(HEB_EINVAL, "heb_bench_butterfly: bad args");
+    if (kind == 1 && p >= (1ull << 42)) return fail(HEB_EINVAL, "heb_bench_butterfly: FP64 engine needs p < 2^42");
+    cudaStream_t st = (cudaStream_t)stream;
+    void *sink;
+    CUDA_TRY(cudaMallocAsync(&sink, 8, st));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (int pass = 0; pass < 2; ++pass) {  // warm-up, then the timed launch
+        const int n = pass ? iters : 4;
+        if (pass) cudaEventRecord(a, st);
+        if (kind == 1) k_bench_bfly_fp<<<blocks, threads, 0, st>>>((double *)sink, (double)p, 1.0 / (double)p, n);
+        else k_bench_bfly_int<<<blocks, threads, 0, st>>>((u64 *)sink, p, n);
+    }
+    cudaEventRecord(b, st);
+    CUDA_TRY(cudaEventSynchronize(b));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    *ms_out = ms;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    CUDA_TRY(cudaFreeAsync(sink, st));
+    return HEB_OK;
+}
