@@ -102,6 +102,22 @@ extern "C" int heb_rescale(heb_ctx *c, heb_ct in, const uint64_t *pt, int64_t ps
 // which equals moddown -> add d -> divide_drop_last of the reference exactly,
 // since every step is an identity mod q_i.
 // =============================================================================
+// Digit layout.  For rows split over a 2-CTA cluster the digits D_j are stored with the
+// even positions first, then the odd ones (MODUP_EO): each CTA of the fused ModUp then
+// owns one contiguous half (one parity class, ntt::forward_split_eo), stages it into
+// shared memory with cp.async while the previous digit's key products run, and the
+// digit is read once per (item, target) instead of twice.
+#ifndef MODUP_EO
+#define MODUP_EO 1
+#endif
+template <int LOGN>
+constexpr bool DIGITS_EO = Row<LOGN>::SP == 2 && MODUP_EO;
+template <int LOGN>
+__device__ __forceinline__ int digit_index(int i) {
+    if constexpr (DIGITS_EO<LOGN>) return ((i & 1) << (LOGN - 1)) | (i >> 1);
+    else return i;
+}
+
 template <int LOGN, int ENG>
 __global__ void ROW_BOUNDS(LOGN) k_ks_head(Ctx K, heb_ct src, int comp, i64 *D, int k,
                                                                    int64_t count, int r0) {
@@ -113,7 +129,10 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_head(Ctx K, heb_ct src, int comp, i64 *D, 
         u64 x[16];
         load16<LOGN>(at(src, b, comp, j, LOGN) + tpos<LOGN>(), x);
         i64 *dst = D + (b * k + j) * (1 << LOGN);
-        inv_any<LOGN, 16, ENG>(K, j, P, sm, x, [&](int i, u64 v) { dst[i] = center(v, P.p); }, true);
+        inv_any<LOGN, 16, ENG>(K, j, P, sm, x, [&](int i, u64 v) {
+            NTT_ASSERT(i >= 0 && i < (1 << LOGN) && b < count && j < k);
+            dst[digit_index<LOGN>(i)] = center(v, P.p);
+        }, true);
     }
 }
 
@@ -136,6 +155,7 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_head(Ctx K, heb_ct src, int comp, i64 *D, 
 // key products are the same residues.  When q_j / 2 < p_t the centred digit already lies
 // in (-p_t, p_t) and needs only a sign fix -- every digit except a wide base digit
 // entering a 40-bit target.
+template <int LOGN>
 struct DigitLoad {
     const i64 *d;
     u64 p, r1s;
@@ -146,7 +166,9 @@ struct DigitLoad {
         if (small) return (u64)v + (v < 0 ? p : 0);
         return signed_mul_const(v, 1, r1s, p);
     }
-    __device__ __forceinline__ u64 operator()(int i) const { return conv(__ldcg(d + i)); }
+    // by position (the parity-split layout is walked through digit_index: only the
+    // fallback paths load by position there)
+    __device__ __forceinline__ u64 operator()(int i) const { return conv(__ldcg(d + digit_index<LOGN>(i))); }
 };
 
 template <int LOGN>
@@ -184,7 +206,7 @@ __global__ void ROW_BOUNDS(LOGN)
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         const i64 *dj = D + (b * k + j) * n;
         u64 y[16];
-        DigitLoad ld(dj, P, K.pi[j].p);
+        DigitLoad<LOGN> ld(dj, P, K.pi[j].p);
         fwd_any<LOGN>(K, gt, P, sm, ld, y);
         store16<LOGN>(V + ((b * (k + 1) + t) * k + j) * n + tpos<LOGN>(), y);
     }
@@ -376,19 +398,25 @@ struct TargetList {
 #ifndef MODUP_KEY_PREFETCH
 #define MODUP_KEY_PREFETCH 0
 #endif
-// Launch order: logical x = target index * G + item-in-group, y = item group.  CTAs are
-// dispatched x-fastest, so each group of G items runs target by target: a target's key
-// rows are shared (in L2) by the G items' CTAs while the group's digits stay in L2.
+#ifndef MODUP_TS_DEFAULT
+#define MODUP_TS_DEFAULT 4
+#endif
+// Launch order: x = target within a set of TS targets, y = item, z = target set.  CTAs are
+// dispatched x-fastest, so the resident CTAs work on ONE set of targets over consecutive
+// items: the set's key rows (TS k rows of 16 N bytes) stay in L2 and are shared by all
+// resident CTAs, while the digits stream through (each item's digits are read by the
+// set's TS CTAs at about the same time).  With every target in flight at once (TS >= all
+// targets, the old order) the cfg4 key (157 MB at k = 18) cycles through the 126 MB L2
+// and every key row comes from HBM (ncu r2b: 136 GB of DRAM reads per 1000-item launch).
 template <int LOGN, int ENG>
 __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MODUP_FP_MINB(LOGN)) k_ks_modup_fused(Ctx K, heb_ct src, int comp, const i64 *D, const ulonglong2 *key,
-                                                  int k, u64 *acc, int64_t count, TargetList tl, int G) {
+                                                  int k, u64 *acc, int64_t count, TargetList tl, int TS) {
     extern __shared__ u64 sm[];
     __shared__ uint32_t tbase;
     // one (item, target) per CTA (pair): the host sizes the grid to cover every item
-    const int L = lbx<LOGN>();
-    const int ti = L / G;
-    const int64_t b = (int64_t)blockIdx.y * G + (L - ti * G);
-    if (b >= count) return;  // both CTAs of a cluster agree
+    const int ti = (int)blockIdx.z * TS + lbx<LOGN>();
+    const int64_t b = blockIdx.y;
+    if (ti >= tl.n) return;  // last (partial) set; both CTAs of a cluster agree
     const int warp = threadIdx.x >> 5;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -412,7 +440,8 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
     {
         bool first = true;
         int staged_for = -1;  // digit whose row (this CTA's part) sits in shared memory
-        if constexpr (Row<LOGN>::SPLIT && MODUP_STAGE_SPLIT && ENG != 0) {
+        constexpr bool EO = DIGITS_EO<LOGN> && ENG != 0;  // parity-split rows, staged digits
+        if constexpr (EO || (Row<LOGN>::SPLIT && MODUP_STAGE_SPLIT && ENG != 0)) {
             // split rows only ever transform from staged digits: stage the first one now
             const int j0 = t == 0 ? 1 : 0;
             if (j0 < k) {
@@ -432,7 +461,7 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
                 }
             } else {
                 const i64 *dj = D + (b * k + j) * n;
-                DigitLoad ld(dj, P, K.pi[j].p);
+                DigitLoad<LOGN> ld(dj, P, K.pi[j].p);
                 if constexpr (ENG == 0) {
                     fwd_any<LOGN>(K, gt, P, sm, ld, y);
                 } else {
@@ -441,7 +470,15 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
                         const ntt::FpArithRaw ar(P.pd, P.pinvd);
                         double *s2 = reinterpret_cast<double *>(sm);
                         const double *tw = K.twf + ((size_t)gt << LOGN);
-                        if constexpr (Row<LOGN>::SPLIT) {
+                        if constexpr (EO) {
+                            asm volatile("cp.async.wait_all;" ::: "memory");
+                            __syncthreads();
+                            first_group_positions<LL>([&](int i) {
+                                const int q = ntt::pad(i);
+                                s2[q] = ntt::u2d(ld.conv(reinterpret_cast<const i64 *>(sm)[q]));
+                            });
+                            ntt::forward_split_eo<LL, 16>(ar, s2, tw, y, rpart<LOGN>());
+                        } else if constexpr (Row<LOGN>::SPLIT) {
                             if constexpr (MODUP_STAGE_SPLIT) ntt::forward_split_staged<LL, 16, Row<LOGN>::SP>(ar, s2, tw, ld, y, rpart<LOGN>());
                             else ntt::forward_split<LL, 16, Row<LOGN>::SP>(ar, s2, tw, ld, y, rpart<LOGN>());
                         } else if (MODUP_STAGE && staged) {
@@ -458,7 +495,15 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
                     } else {
                         const ntt::IntArith ar(P.p);
                         const ulonglong2 *tw = K.tw + ((size_t)gt << LOGN);
-                        if constexpr (Row<LOGN>::SPLIT) {
+                        if constexpr (EO) {
+                            asm volatile("cp.async.wait_all;" ::: "memory");
+                            __syncthreads();
+                            first_group_positions<LL>([&](int i) {
+                                const int q = ntt::pad(i);
+                                sm[q] = ld.conv(reinterpret_cast<const i64 *>(sm)[q]);
+                            });
+                            ntt::forward_split_eo<LL, 16>(ar, sm, tw, y, rpart<LOGN>());
+                        } else if constexpr (Row<LOGN>::SPLIT) {
                             if constexpr (MODUP_STAGE_SPLIT) ntt::forward_split_staged<LL, 16, Row<LOGN>::SP>(ar, sm, tw, ld, y, rpart<LOGN>());
                             else ntt::forward_split<LL, 16, Row<LOGN>::SP>(ar, sm, tw, ld, y, rpart<LOGN>());
                         } else if (MODUP_STAGE_INT && staged) {
@@ -474,12 +519,14 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
                         }
                     }
                     // stage the next digit's row (this CTA's part) during the key products
-                    constexpr bool stage_on = Row<LOGN>::SPLIT ? MODUP_STAGE_SPLIT : (ENG == 1 ? MODUP_STAGE : MODUP_STAGE_INT);
+                    constexpr bool stage_on = EO || (Row<LOGN>::SPLIT ? MODUP_STAGE_SPLIT : (ENG == 1 ? MODUP_STAGE : MODUP_STAGE_INT));
                     if constexpr (stage_on) {
                         int jn = j + 1;
                         if (jn == t) ++jn;
                         if (jn < k) {
-                            __syncthreads();  // every thread has read the transform's output
+                            // every thread has read the transform's output (parity-split
+                            // rows: forward_split_eo ended with a cluster barrier)
+                            if constexpr (!EO) __syncthreads();
                             stage_row_async<LL>(sm, D + (b * k + jn) * n + hoff);
                             staged_for = jn;
                         }
@@ -846,7 +893,8 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
     PREP_ENGINES(k_ks_down_rescale_tail, sm);
     PREP_ENGINES(k_ks_down_tail, sm);
     const int k = level + 1, n = c->n;
-    const int64_t chunk = c->chunk > 0 ? c->chunk : count;
+    // the fused ModUp gives every item of a chunk its own grid row (gridDim.y <= 65535)
+    const int64_t chunk = std::min<int64_t>(c->chunk > 0 ? c->chunk : count, 65535);
     const int64_t cmax = std::min<int64_t>(chunk, count);
     // ModUp sub-chunk: enough (item, t, j) transforms for ~8 CTA waves, V kept small
     static const int64_t target_ctas = [] {
@@ -894,14 +942,17 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
                 l.t[l.n++] = (signed char)t;
                 tl_all.t[tl_all.n++] = (signed char)t;
             }
-            static const int G_env = [] {
-                const char *e = getenv("HEB_MODUP_G");
+            // targets per set (HEB_MODUP_TS; see the kernel): every item gets its own CTA row
+            static const int TS_env = [] {
+                const char *e = getenv("HEB_MODUP_TS");
                 return e ? std::max(1, atoi(e)) : 0;
             }();
-            // every (item, target) gets its own CTA (pair): G * 65535 >= cnt
-            const int G = (int)std::min<int64_t>(
-                cnt, std::max<int64_t>((cnt + 65534) / 65535, G_env > 0 ? G_env : 1));
-            const unsigned gyg = (unsigned)((cnt + G - 1) / G);
+            const int TS = TS_env > 0 ? TS_env : MODUP_TS_DEFAULT;
+            auto mgrid = [&](const TargetList &l) {
+                const int ts = std::min(TS, l.n);
+                return dim3((unsigned)ts, (unsigned)cnt, (unsigned)((l.n + ts - 1) / ts));
+            };
+            auto mts = [&](const TargetList &l) { return std::min(TS, l.n); };
             if (MODUP_ENGINES_SPLIT) {
                 // the integer-target and FP64-target launches are independent (disjoint acc
                 // rows): the integer one goes to the stream's side stream so their CTAs share
@@ -913,15 +964,15 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
                 cudaStream_t ist = st;
                 if (concurrent && tl_int.n) CUDA_TRY(side_fork(c, st, &ist));
                 if (tl_int.n)
-                    CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 2>, dim3(tl_int.n * G, gyg), KT<LOGN>, sm, ist, K,
-                                               s, comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt, tl_int, G));
+                    CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 2>, mgrid(tl_int), KT<LOGN>, sm, ist, K,
+                                               s, comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt, tl_int, mts(tl_int)));
                 if (tl_fp.n)
-                    CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 1>, dim3(tl_fp.n * G, gyg), KT<LOGN>, sm, st, K,
-                                               s, comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt, tl_fp, G));
+                    CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 1>, mgrid(tl_fp), KT<LOGN>, sm, st, K,
+                                               s, comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt, tl_fp, mts(tl_fp)));
                 if (concurrent && tl_int.n) CUDA_TRY(side_join(c, st));
             } else {
-                CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 0>, dim3(tl_all.n * G, gyg), KT<LOGN>, sm, st, K, s,
-                                           comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt, tl_all, G));
+                CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 0>, mgrid(tl_all), KT<LOGN>, sm, st, K, s,
+                                           comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt, tl_all, mts(tl_all)));
             }
         }
         for (int64_t s0 = 0; s0 < (fused ? 0 : cnt); s0 += sub) {

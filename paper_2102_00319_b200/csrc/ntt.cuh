@@ -42,6 +42,16 @@
 
 #include "modarith.cuh"
 
+// -DHEB_DEVICE_ASSERT=1: bounds asserts on every shared-memory and twiddle index of the
+// engine and on the callers' global stores (compute-sanitizer is closed on the GPU pool,
+// so this build is the memory checker; see tools/assert_check.sh)
+#if defined(HEB_DEVICE_ASSERT) && HEB_DEVICE_ASSERT
+#include <cassert>
+#define NTT_ASSERT(c) assert(c)
+#else
+#define NTT_ASSERT(c) ((void)0)
+#endif
+
 namespace ntt {
 
 HD int pad(int i) { return i + (i >> 4); }
@@ -163,7 +173,8 @@ struct FpArithRawIO : FpArithRaw {
 
 // ---------------------------------------------------------------- forward ----
 // One forward group: radix 2^RB covering stages S0 .. S0+RB-1.
-// SRC: 0 = functor load, 1 = shared memory.  DST: 0 = shared memory, 1 = registers.
+// SRC: 0 = functor load, 1 = shared memory.  DST: 0 = shared memory, 1 = registers (line
+// pairs), 2 = shared memory in place, natural order, for the last group (LB = 0).
 template <int LOGN, int E, int RB, int S0, int SRC, int DST, class A, class Load>
 HD void fwd_group(const A &ar, typename A::V *sm, const typename A::W *__restrict__ tw, int c0, Load &load,
                   u64 (&out)[E]) {
@@ -183,6 +194,7 @@ HD void fwd_group(const A &ar, typename A::V *sm, const typename A::W *__restric
 #pragma unroll
         for (int m = 0; m < R; ++m) {
             const int idx = base + (m << LB);
+            NTT_ASSERT(idx >= 0 && idx < S::N);
             if constexpr (SRC == 0) x[m] = ar.in(load(idx));
             else x[m] = sm[pad(idx)];
         }
@@ -192,6 +204,7 @@ HD void fwd_group(const A &ar, typename A::V *sm, const typename A::W *__restric
 #pragma unroll
             for (int m = 0; m < R; ++m) {
                 if (m & half) continue;
+                NTT_ASSERT((c0 << (S0 + q)) + (uhigh << q) + (m >> (RB - q)) < 4 * S::N && uhigh < (1 << S0));
                 const auto w = __ldg(tw + (c0 << (S0 + q)) + (uhigh << q) + (m >> (RB - q)));
                 ar.fwd(x[m], x[m + half], w);
                 if constexpr (A::THROTTLE > 0) {
@@ -206,7 +219,14 @@ HD void fwd_group(const A &ar, typename A::V *sm, const typename A::W *__restric
             for (int m = 0; m < R; ++m) sm[pad(base + m)] = x[m];
             __syncthreads();
 #pragma unroll
-            for (int m = 0; m < R; ++m) out[m] = ar.out_fwd(sm[pad(lpos(tid, m, S::T))]);
+            for (int m = 0; m < R; ++m) {
+                NTT_ASSERT(lpos(tid, m, S::T) < S::N && tid < S::T);
+                out[m] = ar.out_fwd(sm[pad(lpos(tid, m, S::T))]);
+            }
+        } else if constexpr (DST == 2) {
+            static_assert(LB == 0, "in-place output is for the last group");
+#pragma unroll
+            for (int m = 0; m < R; ++m) sm[pad(base + m)] = x[m];
         } else {
 #pragma unroll
             for (int m = 0; m < R; ++m) sm[pad(base + (m << LB))] = x[m];
@@ -214,22 +234,23 @@ HD void fwd_group(const A &ar, typename A::V *sm, const typename A::W *__restric
     }
 }
 
-template <int LOGN, int E, int GI, bool FS, class A, class Load>
+template <int LOGN, int E, int GI, bool FS, int LASTDST, class A, class Load>
 HD void fwd_main_groups(const A &ar, typename A::V *sm, const typename A::W *__restrict__ tw, int c0, Load &load,
                         u64 (&out)[E]) {
     using S = Shape<LOGN, E>;
     constexpr int S0 = S::REM + S::LOGE * GI;
     constexpr bool first = (S0 == 0) && !FS;
     constexpr bool last = (GI == S::G - 1);
-    fwd_group<LOGN, E, S::LOGE, S0, first ? 0 : 1, last ? 1 : 0>(ar, sm, tw, c0, load, out);
+    fwd_group<LOGN, E, S::LOGE, S0, first ? 0 : 1, last ? LASTDST : 0>(ar, sm, tw, c0, load, out);
     if constexpr (!last) {
         __syncthreads();
-        fwd_main_groups<LOGN, E, GI + 1, FS>(ar, sm, tw, c0, load, out);
+        fwd_main_groups<LOGN, E, GI + 1, FS, LASTDST>(ar, sm, tw, c0, load, out);
     }
 }
 
 // FS: the input is already in shared memory (split rows) instead of behind `load`.
-template <int LOGN, int E, bool FS, class A, class Load>
+// LASTDST: 1 = results in registers (line pairs), 2 = left in shared memory (natural order).
+template <int LOGN, int E, bool FS, int LASTDST = 1, class A, class Load>
 __device__ void forward_core(const A &ar, typename A::V *sm, const typename A::W *__restrict__ tw, int c0, Load load,
                              u64 (&out)[E]) {
     using S = Shape<LOGN, E>;
@@ -238,7 +259,7 @@ __device__ void forward_core(const A &ar, typename A::V *sm, const typename A::W
         fwd_group<LOGN, E, S::REM, 0, FS ? 1 : 0, 0>(ar, sm, tw, c0, load, out);
         __syncthreads();
     }
-    fwd_main_groups<LOGN, E, 0, FS>(ar, sm, tw, c0, load, out);
+    fwd_main_groups<LOGN, E, 0, FS, LASTDST>(ar, sm, tw, c0, load, out);
 }
 
 // Forward NTT of one row held by one CTA.
@@ -358,6 +379,44 @@ __device__ void forward_split_staged(const A &ar, typename A::V *sm, const typen
     split_cross_and_local<LL, E, SP>(ar, sm, tw, out, r);
 }
 
+// Forward NTT of a 2^(LL+1) row split over a 2-CTA cluster by the PARITY of the position:
+// CTA r holds positions 2j' + r at local index j' of its shared memory (already converted
+// to A::V).  Stage s < LL pairs positions that differ in bit LL - s >= 1, so it stays
+// inside a parity class and is stage s of a 2^LL transform over the local indices with
+// the row's own twiddles (block j >> (LL + 1 - s) = j' >> (LL - s)): the local engine
+// runs unchanged with c0 = 1.  Only the last stage crosses the CTAs: it pairs (2b, 2b + 1)
+// = (CTA 0's b, CTA 1's b) with twiddle tw[2^LL + b].  CTA r finishes the pairs
+// b in [r 2^(LL-1), (r+1) 2^(LL-1)) -- one value local, one read through distributed
+// shared memory -- which are exactly positions r 2^LL + lpos(t, m) of the row.  Every
+// input element is read by one CTA only (forward_split reads each column twice) and no
+// butterfly is computed twice.  The closing cluster barrier keeps each CTA's shared
+// memory alive until its peer has read it.
+template <int LL, int E = 16, class A>
+__device__ void forward_split_eo(const A &ar, typename A::V *sm, const typename A::W *__restrict__ tw, u64 (&out)[E],
+                                 int r) {
+    using S = Shape<LL, E>;
+    using V = typename A::V;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    int dummy = 0;
+    auto noload = [&](int) { return (u64)dummy; };
+    forward_core<LL, E, true, 2>(ar, sm, tw, 1, noload, out);
+    cluster.sync();  // both parity classes are complete
+    const V *pe = cluster.map_shared_rank(sm, 0);
+    const V *po = cluster.map_shared_rank(sm, 1);
+    constexpr int H = (1 << LL) / 2;
+    static_assert(H == (E / 2) * S::T, "E/2 pairs per thread");
+#pragma unroll
+    for (int i = 0; i < E / 2; ++i) {
+        const int b = r * H + (int)threadIdx.x + S::T * i;
+        V u = pe[pad(b)], v = po[pad(b)];
+        ar.fwd(u, v, __ldg(tw + (1 << LL) + b));
+        out[2 * i] = ar.out_fwd(u);
+        out[2 * i + 1] = ar.out_fwd(v);
+    }
+    cluster.sync();  // the peer has read this CTA's results: shared memory may be reused
+}
+
 // ---------------------------------------------------------------- inverse ----
 // SRC: 1 = registers, 0 = shared memory.  DST: 0 = shared memory, 1 = functor store.
 // LASTS: this group contains global stage 0 (fold n^-1 and canonicalise).
@@ -381,7 +440,10 @@ HD void inv_group(const A &ar, typename A::V *sm, const typename A::W *__restric
             static_assert(UPT == 1 && R == E && LB == 0, "register input needs one radix-E unit per thread");
             // line-pair order in registers -> this unit's contiguous positions
 #pragma unroll
-            for (int m = 0; m < R; ++m) sm[pad(lpos(tid, m, S::T))] = ar.in(in[m]);
+            for (int m = 0; m < R; ++m) {
+                NTT_ASSERT(lpos(tid, m, S::T) < S::N && tid < S::T);
+                sm[pad(lpos(tid, m, S::T))] = ar.in(in[m]);
+            }
             __syncthreads();
 #pragma unroll
             for (int m = 0; m < R; ++m) x[m] = sm[pad(base + m)];
@@ -398,6 +460,7 @@ HD void inv_group(const A &ar, typename A::V *sm, const typename A::W *__restric
                 if (LASTS && S0 + q == 0) {
                     ar.inv_last(x[m], x[m + half], last_u, last_v);
                 } else {
+                    NTT_ASSERT((c0 << (S0 + q)) + (uhigh << q) + (m >> (RB - q)) < 4 * S::N && uhigh < (1 << S0));
                     const auto w = __ldg(itw + (c0 << (S0 + q)) + (uhigh << q) + (m >> (RB - q)));
                     ar.inv(x[m], x[m + half], w);
                     if constexpr (A::THROTTLE > 0) {
@@ -408,7 +471,10 @@ HD void inv_group(const A &ar, typename A::V *sm, const typename A::W *__restric
         }
         if constexpr (DST == 1) {
 #pragma unroll
-            for (int m = 0; m < R; ++m) store(base + (m << LB), ar.out_inv(x[m]));
+            for (int m = 0; m < R; ++m) {
+                NTT_ASSERT(base + (m << LB) >= 0 && base + (m << LB) < S::N);
+                store(base + (m << LB), ar.out_inv(x[m]));
+            }
         } else {
 #pragma unroll
             for (int m = 0; m < R; ++m) sm[pad(base + (m << LB))] = ar.to_smem_inv(x[m]);
