@@ -238,7 +238,7 @@ __device__ __forceinline__ void fwd_any(const Ctx &K, int row, const PrimeInfo &
     constexpr int LL = Row<LOGN>::LL;
     if constexpr (ENG == 2) {
         const ntt::IntArith ar(P.p);
-        const ulonglong2 *tw = K.tw + ((size_t)row << LOGN);
+        const ulonglong2 *tw = K.tw + ((size_t)row << (LOGN + ntt::TW_ROW_SHIFT));
         if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, E, Row<LOGN>::SP>(ar, sm, tw, load, out, rpart<LOGN>());
         else ntt::forward<LL, E>(ar, sm, tw, load, out);
         return;
@@ -246,12 +246,12 @@ __device__ __forceinline__ void fwd_any(const Ctx &K, int row, const PrimeInfo &
     if (ENG == 1 || HEB_FPSEL(P.use_fp)) {
         const ntt::FpArith ar(P.pd, P.pinvd);
         double *s = reinterpret_cast<double *>(sm);
-        const double *tw = K.twf + ((size_t)row << LOGN);
+        const double *tw = K.twf + ((size_t)row << (LOGN + ntt::TW_ROW_SHIFT));
         if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, E, Row<LOGN>::SP>(ar, s, tw, load, out, rpart<LOGN>());
         else ntt::forward<LL, E>(ar, s, tw, load, out);
     } else if constexpr (ENG == 0) {
         const ntt::IntArith ar(P.p);
-        const ulonglong2 *tw = K.tw + ((size_t)row << LOGN);
+        const ulonglong2 *tw = K.tw + ((size_t)row << (LOGN + ntt::TW_ROW_SHIFT));
         if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, E, Row<LOGN>::SP>(ar, sm, tw, load, out, rpart<LOGN>());
         else ntt::forward<LL, E>(ar, sm, tw, load, out);
     }
@@ -264,7 +264,7 @@ __device__ __forceinline__ void inv_any(const Ctx &K, int row, const PrimeInfo &
     const LastConst &lc = K.last[row];
     if constexpr (ENG == 2) {
         const ntt::IntArith ar(P.p);
-        const ulonglong2 *itw = K.itw + ((size_t)row << LOGN);
+        const ulonglong2 *itw = K.itw + ((size_t)row << (LOGN + ntt::TW_ROW_SHIFT));
         const ulonglong2 u = std_out ? lc.u_std : lc.u_plain, v = std_out ? lc.v_std : lc.v_plain;
         if constexpr (Row<LOGN>::SPLIT) ntt::inverse_split<LL, E, Row<LOGN>::SP>(ar, sm, itw, in, store, u, v, rpart<LOGN>());
         else ntt::inverse<LL, E>(ar, sm, itw, in, store, u, v);
@@ -273,13 +273,13 @@ __device__ __forceinline__ void inv_any(const Ctx &K, int row, const PrimeInfo &
     if (ENG == 1 || HEB_FPSEL(P.use_fp)) {
         const ntt::FpArith ar(P.pd, P.pinvd);
         double *s = reinterpret_cast<double *>(sm);
-        const double *itw = K.itwf + ((size_t)row << LOGN);
+        const double *itw = K.itwf + ((size_t)row << (LOGN + ntt::TW_ROW_SHIFT));
         const double u = std_out ? lc.fu_std : lc.fu_plain, v = std_out ? lc.fv_std : lc.fv_plain;
         if constexpr (Row<LOGN>::SPLIT) ntt::inverse_split<LL, E, Row<LOGN>::SP>(ar, s, itw, in, store, u, v, rpart<LOGN>());
         else ntt::inverse<LL, E>(ar, s, itw, in, store, u, v);
     } else if constexpr (ENG == 0) {
         const ntt::IntArith ar(P.p);
-        const ulonglong2 *itw = K.itw + ((size_t)row << LOGN);
+        const ulonglong2 *itw = K.itw + ((size_t)row << (LOGN + ntt::TW_ROW_SHIFT));
         const ulonglong2 u = std_out ? lc.u_std : lc.u_plain, v = std_out ? lc.v_std : lc.v_plain;
         if constexpr (Row<LOGN>::SPLIT) ntt::inverse_split<LL, E, Row<LOGN>::SP>(ar, sm, itw, in, store, u, v, rpart<LOGN>());
         else ntt::inverse<LL, E>(ar, sm, itw, in, store, u, v);
@@ -380,11 +380,11 @@ static cudaError_t launch_by_engine(const heb_ctx *cc, K0 k0, K1 k1, K2 k2, int 
 
 template <int LOGN>
 __device__ __forceinline__ const ulonglong2 *tw_row(const Ctx &k, int row) {
-    return k.tw + ((size_t)row << LOGN);
+    return k.tw + ((size_t)row << (LOGN + ntt::TW_ROW_SHIFT));
 }
 template <int LOGN>
 __device__ __forceinline__ const ulonglong2 *itw_row(const Ctx &k, int row) {
-    return k.itw + ((size_t)row << LOGN);
+    return k.itw + ((size_t)row << (LOGN + ntt::TW_ROW_SHIFT));
 }
 
 // a thread's 16 line-pair positions starting at src = row + tpos(): 16-byte accesses,

@@ -89,8 +89,10 @@ extern "C" int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows
         c->flush = lim > 64 ? 64 : (int)lim;
     }
     std::vector<PrimeInfo> pi(num_rows);
-    std::vector<ulonglong2> tw((size_t)num_rows * n), itw((size_t)num_rows * n);
-    std::vector<double> twf((size_t)num_rows * n), itwf((size_t)num_rows * n);
+    // 4n entries per row: reference order, then the lane-major regions (ntt.cuh, TW_ROW_SHIFT)
+    const size_t rs = (size_t)n << ntt::TW_ROW_SHIFT;
+    std::vector<ulonglong2> tw((size_t)num_rows * rs, make_ulonglong2(0, 0)), itw((size_t)num_rows * rs, make_ulonglong2(0, 0));
+    std::vector<double> twf((size_t)num_rows * rs, 0.0), itwf((size_t)num_rows * rs, 0.0);
     std::vector<LastConst> last(num_rows);
     const char *fp_env = getenv("HEB_DISABLE_FP64_NTT");
     const bool fp_disabled = fp_env && fp_env[0] == '1';
@@ -120,10 +122,25 @@ extern "C" int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows
         for (int i = 1; i < n; ++i) pw[i] = mulmod_h(pw[i - 1], g, p);
         for (int i = 0; i < n; ++i) {
             u64 w = pw[brv_h((u32)i, log_n)];
-            tw[(size_t)r * n + i] = shoup_pair(w, p);
-            itw[(size_t)r * n + i] = shoup_pair(invmod_h(w, p), p);
+            tw[(size_t)r * rs + i] = shoup_pair(w, p);
+            itw[(size_t)r * rs + i] = shoup_pair(invmod_h(w, p), p);
         }
-        const u64 it1 = itw[(size_t)r * n + 1].x;
+        // lane-major copies of the last radix-16 group's twiddles: first stage S = log_n - 4
+        // at [n, 2n), S = log_n - 5 at [2n, 3n)
+        for (int region = 1; region <= 2; ++region) {
+            const int S = log_n - 3 - region;
+            if (S < 0) continue;
+            const size_t base = (size_t)r * rs + (size_t)region * n;
+            for (int q = 0; q < 4; ++q)
+                for (int i = 0; i < (1 << q); ++i)
+                    for (int g = 0; g < (1 << S); ++g) {
+                        const size_t src = (size_t)r * rs + ((((size_t)1 << S) + g) << q) + i;
+                        const size_t dst = base + ((size_t)((1 << q) - 1 + i) << S) + g;
+                        tw[dst] = tw[src];
+                        itw[dst] = itw[src];
+                    }
+        }
+        const u64 it1 = itw[(size_t)r * rs + 1].x;
         last[r].u_plain = shoup_pair(q.ninv, p);
         last[r].v_plain = shoup_pair(mulmod_h(it1, q.ninv, p), p);
         last[r].u_std = shoup_pair(q.ninv_rinv, p);
@@ -134,9 +151,9 @@ extern "C" int heb_ctx_create(heb_ctx **out, int device, int log_n, int num_rows
         q.use_fp = (p < (1ull << 42)) && !fp_disabled;
         c->row_fp.push_back(q.use_fp ? 1 : 0);
         auto fpair = [&](u64 w) { return (double)w; };
-        for (int i = 0; i < n; ++i) {
-            twf[(size_t)r * n + i] = fpair(tw[(size_t)r * n + i].x);
-            itwf[(size_t)r * n + i] = fpair(itw[(size_t)r * n + i].x);
+        for (size_t i = 0; i < rs; ++i) {
+            twf[(size_t)r * rs + i] = fpair(tw[(size_t)r * rs + i].x);
+            itwf[(size_t)r * rs + i] = fpair(itw[(size_t)r * rs + i].x);
         }
         last[r].fu_plain = fpair(last[r].u_plain.x);
         last[r].fv_plain = fpair(last[r].v_plain.x);

@@ -34,6 +34,10 @@ constexpr int FG = CONV_FGF;  // filters per CTA group
 #ifndef CONV_MINB
 #define CONV_MINB 2
 #endif
+// taps whose inputs are in flight ahead of the one being multiplied (FP64 split-limb body)
+#ifndef CONV_AHEAD
+#define CONV_AHEAD 1
+#endif
 
 // One CTA = (row r, XC positions from bx * XC, filter group): integer rows (and, without
 // the split-limb path, FP64 rows with one exact FP64 modular product per term).
@@ -240,14 +244,31 @@ __device__ __forceinline__ void conv_body_limbs(double *wl, const Ctx &K, const 
         // taps in (c, p, q) order; the next tap's inputs are loaded before this tap's math
         const u64 *base = A.data + ((int64_t)(i * s) * n + j * s) * A.ct_stride + roff;
         u64 na0 = __ldg(base), na1 = __ldg(base + A.comp_stride);
+#if CONV_AHEAD == 2
+        u64 nb0 = 0, nb1 = 0;
+        if (taps > 1) {
+            nb0 = __ldg(base + toff[1]);
+            nb1 = __ldg(base + toff[1] + A.comp_stride);
+        }
+#endif
         for (int tap = 0; tap < taps; ++tap) {
             {
                 const u64 a0 = na0, a1 = na1;
+#if CONV_AHEAD == 2
+                na0 = nb0;
+                na1 = nb1;
+                if (tap + 2 < taps) {
+                    const u64 *ap = base + toff[tap + 2];
+                    nb0 = __ldg(ap);
+                    nb1 = __ldg(ap + A.comp_stride);
+                }
+#else
                 if (tap + 1 < taps) {
                     const u64 *ap = base + toff[tap + 1];
                     na0 = __ldg(ap);
                     na1 = __ldg(ap + A.comp_stride);
                 }
+#endif
                 {
                     const double a0h = ntt::u2d(a0 >> 20), a0l = ntt::u2d(a0 & M20);
                     const double a1h = ntt::u2d(a1 >> 20), a1l = ntt::u2d(a1 & M20);

@@ -1,4 +1,6 @@
 // keyswitch.cu -- rescale, relinearisation (key switch + ModDown + rescale) and rotation.
+#include <type_traits>
+
 #include "common.cuh"
 
 // =============================================================================
@@ -131,7 +133,10 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_head(Ctx K, heb_ct src, int comp, i64 *D, 
         i64 *dst = D + (b * k + j) * (1 << LOGN);
         inv_any<LOGN, 16, ENG>(K, j, P, sm, x, [&](int i, u64 v) {
             NTT_ASSERT(i >= 0 && i < (1 << LOGN) && b < count && j < k);
-            dst[digit_index<LOGN>(i)] = center(v, P.p);
+            // digits of FP64-engine primes (< 2^42) are stored as the double of the centred
+            // value (exact): the FP64 ModUp targets transform them as they are (DigitLoad)
+            dst[digit_index<LOGN>(i)] =
+                P.use_fp ? (i64)__double_as_longlong(ntt::u2d(v) - (v > (P.p >> 1) ? P.pd : 0.0)) : center(v, P.p);
         }, true);
     }
 }
@@ -159,10 +164,15 @@ template <int LOGN>
 struct DigitLoad {
     const i64 *d;
     u64 p, r1s;
-    bool small;
-    __device__ __forceinline__ DigitLoad(const i64 *d_, const PrimeInfo &P, u64 qj)
-        : d(d_), p(P.p), r1s(P.r1s), small((qj >> 1) < P.p) {}
+    bool small, dbl;  // dbl: the digit's words are doubles (its prime runs on the FP64 engine, see k_ks_head)
+    __device__ __forceinline__ DigitLoad(const i64 *d_, const PrimeInfo &P, const PrimeInfo &Pj)
+        : d(d_), p(P.p), r1s(P.r1s), small((Pj.p >> 1) < P.p), dbl(Pj.use_fp != 0) {}
+    // stored word -> canonical residue mod p
     __device__ __forceinline__ u64 conv(i64 v) const {
+        if (dbl) {  // exact integer |x| < 2^41: x + 1.5 * 2^52 keeps 2^51 + x in the mantissa field
+            const long long b = __double_as_longlong(__longlong_as_double(v) + FP_MAGIC);
+            v = (b & ((1ll << 52) - 1)) - (1ll << 51);
+        }
         if (small) return (u64)v + (v < 0 ? p : 0);
         return signed_mul_const(v, 1, r1s, p);
     }
@@ -206,7 +216,7 @@ __global__ void ROW_BOUNDS(LOGN)
     for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
         const i64 *dj = D + (b * k + j) * n;
         u64 y[16];
-        DigitLoad<LOGN> ld(dj, P, K.pi[j].p);
+        DigitLoad<LOGN> ld(dj, P, K.pi[j]);
         fwd_any<LOGN>(K, gt, P, sm, ld, y);
         store16<LOGN>(V + ((b * (k + 1) + t) * k + j) * n + tpos<LOGN>(), y);
     }
@@ -237,55 +247,94 @@ __device__ __forceinline__ void tmem_ld8(uint32_t a, uint32_t (&v)[8]) {
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// key rows are streamed once per CTA: keep them out of L1 (the transform's twiddles live there)
+__device__ __forceinline__ double2 ld_key(const double2 *p) {
+    double2 v;
+    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ ulonglong2 ld_key(const ulonglong2 *p) {
+    ulonglong2 v;
+    asm("ld.global.nc.L1::no_allocate.v2.u64 {%0,%1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
+    return v;
+}
+
 // accumulate y (*) key over this thread's 16 line-pair positions, 4 positions per TMEM access
-// (RAW: FP64 rows hand y over as raw double bit patterns, FpArithRaw)
+// (RAW: FP64 rows hand y over as raw double bit patterns, FpArithRaw).  The tcgen05 asm
+// statements are compiler barriers for memory operations, so the key values of the next
+// (q, c) step are loaded explicitly before the current step's TMEM round trip
+// (MODUP_KEY_AHEAD steps ahead): their L2 latency then overlaps the products instead of
+// adding up over the 8 steps.
+#ifndef MODUP_KEY_AHEAD
+#define MODUP_KEY_AHEAD 1
+#endif
+#ifndef MODUP_KEY_AHEAD_INT
+#define MODUP_KEY_AHEAD_INT 0  // 64 bytes of key per step: more spills than the load-ahead saves
+#endif
 template <int LOGN, bool FP, bool RAW = false>
 __device__ __forceinline__ void modup_acc(uint32_t ta, const u64 (&y)[16], const ulonglong2 *keyrow, int pos,
                                           bool first, const PrimeInfo &P) {
     const int n = 1 << LOGN;
     constexpr int T = KT<LOGN>;
+    using KV = typename std::conditional<FP, double2, ulonglong2>::type;
+    constexpr int NK = FP ? 2 : 4;  // 16-byte key words per step (two position pairs)
+    auto load_step = [&](int it, KV (&kv)[NK]) {
+        const int q = it >> 1, c = it & 1;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {  // positions m = 4q .. 4q+3 = pairs 2q, 2q+1
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            uint32_t w[8];
-            if (!first) tmem_ld8(ta + 32 * c + 8 * q, w);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int i = 2 * q + h;  // pair index: positions pos + 2T i (+1)
-                const int off = pos + 2 * T * i;
-                if constexpr (FP) {
-                    const double *kd = reinterpret_cast<const double *>(keyrow) + (size_t)c * n;
-                    const double2 kv = __ldg(reinterpret_cast<const double2 *>(kd + off));
-                    const double y0 = RAW ? __longlong_as_double((long long)y[2 * i]) : ntt::u2d(y[2 * i]);
-                    const double y1 = RAW ? __longlong_as_double((long long)y[2 * i + 1]) : ntt::u2d(y[2 * i + 1]);
-                    double a0 = ntt::fmul(y0, kv.x, P.pd, P.pinvd);
-                    double a1 = ntt::fmul(y1, kv.y, P.pd, P.pinvd);
-                    if (!first) {
-                        a0 += __hiloint2double(w[4 * h + 1], w[4 * h]);
-                        a1 += __hiloint2double(w[4 * h + 3], w[4 * h + 2]);
-                    }
-                    w[4 * h] = __double2loint(a0);
-                    w[4 * h + 1] = __double2hiint(a0);
-                    w[4 * h + 2] = __double2loint(a1);
-                    w[4 * h + 3] = __double2hiint(a1);
-                } else {
-                    const ulonglong2 *kp = keyrow + (size_t)c * n + off;
-                    const ulonglong2 k0 = __ldg(kp), k1 = __ldg(kp + 1);
-                    u64 a0 = shoup_lazy(y[2 * i], k0.x, k0.y, P.p);
-                    u64 a1 = shoup_lazy(y[2 * i + 1], k1.x, k1.y, P.p);
-                    if (!first) {
-                        a0 = csub(a0 + ((u64)w[4 * h + 1] << 32 | w[4 * h]), 2 * P.p);
-                        a1 = csub(a1 + ((u64)w[4 * h + 3] << 32 | w[4 * h + 2]), 2 * P.p);
-                    }
-                    w[4 * h] = (uint32_t)a0;
-                    w[4 * h + 1] = (uint32_t)(a0 >> 32);
-                    w[4 * h + 2] = (uint32_t)a1;
-                    w[4 * h + 3] = (uint32_t)(a1 >> 32);
-                }
+        for (int h = 0; h < 2; ++h) {
+            const int off = pos + 2 * T * (2 * q + h);
+            if constexpr (FP) {
+                const double *kd = reinterpret_cast<const double *>(keyrow) + (size_t)c * n;
+                kv[h] = ld_key(reinterpret_cast<const double2 *>(kd + off));
+            } else {
+                const ulonglong2 *kp = keyrow + (size_t)c * n + off;
+                kv[2 * h] = ld_key(kp);
+                kv[2 * h + 1] = ld_key(kp + 1);
             }
-            tmem_st8(ta + 32 * c + 8 * q, w);
         }
+    };
+    // ring of AH + 1 key buffers; every index below is a compile-time constant after unrolling
+    constexpr int AH = FP ? MODUP_KEY_AHEAD : MODUP_KEY_AHEAD_INT;
+    KV kb[AH + 1][NK];
+#pragma unroll
+    for (int a = 0; a < AH; ++a) load_step(a, kb[a]);
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {  // q = it >> 1: positions m = 4q .. 4q+3 = pairs 2q, 2q+1; c = it & 1
+        const int q = it >> 1, c = it & 1;
+        if (it + AH < 8) load_step(it + AH, kb[(it + AH) % (AH + 1)]);
+        KV(&kv)[NK] = kb[it % (AH + 1)];
+        uint32_t w[8];
+        if (!first) tmem_ld8(ta + 32 * c + 8 * q, w);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int i = 2 * q + h;  // pair index: positions pos + 2T i (+1)
+            if constexpr (FP) {
+                const double y0 = RAW ? __longlong_as_double((long long)y[2 * i]) : ntt::u2d(y[2 * i]);
+                const double y1 = RAW ? __longlong_as_double((long long)y[2 * i + 1]) : ntt::u2d(y[2 * i + 1]);
+                double a0 = ntt::fmul(y0, kv[h].x, P.pd, P.pinvd);
+                double a1 = ntt::fmul(y1, kv[h].y, P.pd, P.pinvd);
+                if (!first) {
+                    a0 += __hiloint2double(w[4 * h + 1], w[4 * h]);
+                    a1 += __hiloint2double(w[4 * h + 3], w[4 * h + 2]);
+                }
+                w[4 * h] = __double2loint(a0);
+                w[4 * h + 1] = __double2hiint(a0);
+                w[4 * h + 2] = __double2loint(a1);
+                w[4 * h + 3] = __double2hiint(a1);
+            } else {
+                u64 a0 = shoup_lazy(y[2 * i], kv[2 * h].x, kv[2 * h].y, P.p);
+                u64 a1 = shoup_lazy(y[2 * i + 1], kv[2 * h + 1].x, kv[2 * h + 1].y, P.p);
+                if (!first) {
+                    a0 = csub(a0 + ((u64)w[4 * h + 1] << 32 | w[4 * h]), 2 * P.p);
+                    a1 = csub(a1 + ((u64)w[4 * h + 3] << 32 | w[4 * h + 2]), 2 * P.p);
+                }
+                w[4 * h] = (uint32_t)a0;
+                w[4 * h + 1] = (uint32_t)(a0 >> 32);
+                w[4 * h + 2] = (uint32_t)a1;
+                w[4 * h + 3] = (uint32_t)(a1 >> 32);
+            }
+        }
+        tmem_st8(ta + 32 * c + 8 * q, w);
     }
     tmem_wait_st();
 }
@@ -461,7 +510,7 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
                 }
             } else {
                 const i64 *dj = D + (b * k + j) * n;
-                DigitLoad<LOGN> ld(dj, P, K.pi[j].p);
+                DigitLoad<LOGN> ld(dj, P, K.pi[j]);
                 if constexpr (ENG == 0) {
                     fwd_any<LOGN>(K, gt, P, sm, ld, y);
                 } else {
@@ -469,14 +518,17 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
                     if constexpr (ENG == 1) {
                         const ntt::FpArithRaw ar(P.pd, P.pinvd);
                         double *s2 = reinterpret_cast<double *>(sm);
-                        const double *tw = K.twf + ((size_t)gt << LOGN);
+                        const double *tw = K.twf + ((size_t)gt << (LOGN + ntt::TW_ROW_SHIFT));
                         if constexpr (EO) {
+                            // the first group reads exactly the words this thread staged; a
+                            // double-format digit is transformed as it lies in shared memory
                             asm volatile("cp.async.wait_all;" ::: "memory");
-                            __syncthreads();
-                            first_group_positions<LL>([&](int i) {
-                                const int q = ntt::pad(i);
-                                s2[q] = ntt::u2d(ld.conv(reinterpret_cast<const i64 *>(sm)[q]));
-                            });
+                            if (!ld.dbl) {
+                                first_group_positions<LL>([&](int i) {
+                                    const int q = ntt::pad(i);
+                                    s2[q] = ntt::u2d(ld.conv(reinterpret_cast<const i64 *>(sm)[q]));
+                                });
+                            }
                             ntt::forward_split_eo<LL, 16>(ar, s2, tw, y, rpart<LOGN>());
                         } else if constexpr (Row<LOGN>::SPLIT) {
                             if constexpr (MODUP_STAGE_SPLIT) ntt::forward_split_staged<LL, 16, Row<LOGN>::SP>(ar, s2, tw, ld, y, rpart<LOGN>());
@@ -484,20 +536,21 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
                         } else if (MODUP_STAGE && staged) {
                             asm volatile("cp.async.wait_all;" ::: "memory");
                             __syncthreads();
-                            first_group_positions<LL>([&](int i) {
-                                const int q = ntt::pad(i);
-                                s2[q] = ntt::u2d(ld.conv(reinterpret_cast<const i64 *>(sm)[q]));
-                            });
+                            if (!ld.dbl) {
+                                first_group_positions<LL>([&](int i) {
+                                    const int q = ntt::pad(i);
+                                    s2[q] = ntt::u2d(ld.conv(reinterpret_cast<const i64 *>(sm)[q]));
+                                });
+                            }
                             ntt::forward_core<LL, 16, true>(ar, s2, tw, 1, ld, y);
                         } else {
                             ntt::forward<LL, 16>(ar, s2, tw, ld, y);
                         }
                     } else {
                         const ntt::IntArith ar(P.p);
-                        const ulonglong2 *tw = K.tw + ((size_t)gt << LOGN);
+                        const ulonglong2 *tw = K.tw + ((size_t)gt << (LOGN + ntt::TW_ROW_SHIFT));
                         if constexpr (EO) {
                             asm volatile("cp.async.wait_all;" ::: "memory");
-                            __syncthreads();
                             first_group_positions<LL>([&](int i) {
                                 const int q = ntt::pad(i);
                                 sm[q] = ld.conv(reinterpret_cast<const i64 *>(sm)[q]);
@@ -802,7 +855,7 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_down_rescale_tail(Ctx K, const u64 *acc, h
         // canonicalise / convert round trip on either side of it
         const ntt::FpArithRawIO fa(pd, pinvd);
         double *s2 = reinterpret_cast<double *>(sm);
-        const double *twf = K.twf + ((size_t)i << LOGN);
+        const double *twf = K.twf + ((size_t)i << (LOGN + ntt::TW_ROW_SHIFT));
         for (int64_t b = blockIdx.y; b < count; b += gridDim.y) {
             const i64 *ap = aP + (b * 2 + c) * n;
             const i64 *cl = cL + (b * 2 + c) * n;

@@ -73,6 +73,34 @@ struct Shape {
     static constexpr int SMEM_WORDS = N + N / 16;
 };
 
+// Twiddle tables hold 4N entries per row (TW_ROW_SHIFT): [0, N) psi^brv(i) in the reference's
+// order; [N, 2N) the entries of the last radix-16 group of the full transform (first stage
+// S = n - 4) regrouped lane-major, P_S[(2^q - 1 + i) 2^S + g] = tw[((2^S + g) << q) + i]
+// for stage S + q, unit g: in that group every thread owns one unit and needs 15
+// twiddles of its own; in the reference order a warp's loads of one (q, i) are strided by
+// 8 * 2^q bytes (up to 16 lines per request), regrouped they are one contiguous 256-byte
+// run (the group was bound by L1 wavefronts, not by the DFMA pipe);  [2N, 3N) the same
+// for S = n - 5, the last local group of a parity-split row (forward_split_eo).
+constexpr int TW_ROW_SHIFT = 2;
+#ifndef NTT_TW_LANE_MAJOR
+#define NTT_TW_LANE_MAJOR 1
+#endif
+// Address of the lane-major twiddles of unit u of this CTA in a last group (LOGN = this
+// CTA's part, first stage S0 = LOGN - 4, c0 = its twiddle base multiplier); the entry of
+// stage S0 + q, butterfly i is at [((1 << q) - 1 + i) * stride].  PERM 1: full-transform
+// group of a row of SP parts (c0 = SP + part); PERM 2: parity-split local group.
+template <int LOGN, int S0, int PERM, class W>
+HD const W *lane_major_tw(const W *__restrict__ tw, int c0, int u, int &stride) {
+    if constexpr (PERM == 2) {
+        stride = 1 << S0;
+        return tw + (size_t)(4 << LOGN) + u;  // row length 2 * 2^LOGN, region [2N, 3N)
+    } else {
+        const int sp = c0 >= 4 ? 4 : (c0 >= 2 ? 2 : 1);
+        stride = sp << S0;
+        return tw + (size_t)(sp << LOGN) + ((c0 - sp) << S0) + u;
+    }
+}
+
 // ---------------------------------------------------------------- arithmetic ----
 struct IntArith {
     using V = u64;
@@ -171,11 +199,39 @@ struct FpArithRawIO : FpArithRaw {
     HD V in(u64 x) const { return __longlong_as_double((long long)x); }
 };
 
+// Barrier over the NT consecutive threads around this thread (NT a power of two).  After
+// the group that starts at stage S0 every later forward stage stays inside blocks of
+// N / 2^S0 positions, and the thread -> unit map keeps a block with the same T / 2^S0
+// consecutive threads in every group, so the exchange between two groups only needs
+// those threads: the whole CTA, one named barrier per NT-thread slice, or just the warp.
+// A CTA that is alone on its SM (N >= 2^14 parts) then stalls as a whole only around the
+// first group and the boundary transposition instead of at every exchange.
+#ifndef NTT_FINE_SYNC
+#define NTT_FINE_SYNC 1
+#endif
+template <int T, int NT>
+HD void sync_slice() {
+    if constexpr (!NTT_FINE_SYNC || NT >= T) {
+        __syncthreads();
+    } else if constexpr (NT <= 32) {
+        __syncwarp();
+    } else if constexpr (T / NT > 4) {  // at most four named barriers (1..4) per CTA
+        sync_slice<T, NT * 2>();
+    } else {
+        // immediate barrier numbers: a register operand makes ptxas reserve all 16 barriers
+        const int s = (int)threadIdx.x / NT;
+        if (s == 0) asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+        else if (s == 1) asm volatile("bar.sync 2, %0;" ::"n"(NT) : "memory");
+        else if (s == 2) asm volatile("bar.sync 3, %0;" ::"n"(NT) : "memory");
+        else asm volatile("bar.sync 4, %0;" ::"n"(NT) : "memory");
+    }
+}
+
 // ---------------------------------------------------------------- forward ----
 // One forward group: radix 2^RB covering stages S0 .. S0+RB-1.
 // SRC: 0 = functor load, 1 = shared memory.  DST: 0 = shared memory, 1 = registers (line
 // pairs), 2 = shared memory in place, natural order, for the last group (LB = 0).
-template <int LOGN, int E, int RB, int S0, int SRC, int DST, class A, class Load>
+template <int LOGN, int E, int RB, int S0, int SRC, int DST, int PERM, class A, class Load>
 HD void fwd_group(const A &ar, typename A::V *sm, const typename A::W *__restrict__ tw, int c0, Load &load,
                   u64 (&out)[E]) {
     using S = Shape<LOGN, E>;
@@ -190,6 +246,10 @@ HD void fwd_group(const A &ar, typename A::V *sm, const typename A::W *__restric
         const int ulow = u & ((1 << LB) - 1);
         const int uhigh = u >> LB;
         const int base = (uhigh << (LOGN - S0)) | ulow;
+        constexpr bool LANE_MAJOR = NTT_TW_LANE_MAJOR && PERM != 0 && LB == 0 && RB == 4 && UPT == 1;
+        int lm_stride = 0;
+        const typename A::W *lm = nullptr;
+        if constexpr (LANE_MAJOR) lm = lane_major_tw<LOGN, S0, PERM>(tw, c0, u, lm_stride);
         V x[R];
 #pragma unroll
         for (int m = 0; m < R; ++m) {
@@ -205,7 +265,9 @@ HD void fwd_group(const A &ar, typename A::V *sm, const typename A::W *__restric
             for (int m = 0; m < R; ++m) {
                 if (m & half) continue;
                 NTT_ASSERT((c0 << (S0 + q)) + (uhigh << q) + (m >> (RB - q)) < 4 * S::N && uhigh < (1 << S0));
-                const auto w = __ldg(tw + (c0 << (S0 + q)) + (uhigh << q) + (m >> (RB - q)));
+                typename A::W w;
+                if constexpr (LANE_MAJOR) w = __ldg(lm + ((1 << q) - 1 + (m >> (RB - q))) * lm_stride);
+                else w = __ldg(tw + (c0 << (S0 + q)) + (uhigh << q) + (m >> (RB - q)));
                 ar.fwd(x[m], x[m + half], w);
                 if constexpr (A::THROTTLE > 0) {
                     if ((m % A::THROTTLE) == A::THROTTLE - 1) asm volatile("" ::: "memory");
@@ -234,32 +296,33 @@ HD void fwd_group(const A &ar, typename A::V *sm, const typename A::W *__restric
     }
 }
 
-template <int LOGN, int E, int GI, bool FS, int LASTDST, class A, class Load>
+template <int LOGN, int E, int GI, bool FS, int LASTDST, int PERM, class A, class Load>
 HD void fwd_main_groups(const A &ar, typename A::V *sm, const typename A::W *__restrict__ tw, int c0, Load &load,
                         u64 (&out)[E]) {
     using S = Shape<LOGN, E>;
     constexpr int S0 = S::REM + S::LOGE * GI;
     constexpr bool first = (S0 == 0) && !FS;
     constexpr bool last = (GI == S::G - 1);
-    fwd_group<LOGN, E, S::LOGE, S0, first ? 0 : 1, last ? LASTDST : 0>(ar, sm, tw, c0, load, out);
+    fwd_group<LOGN, E, S::LOGE, S0, first ? 0 : 1, last ? LASTDST : 0, PERM>(ar, sm, tw, c0, load, out);
     if constexpr (!last) {
-        __syncthreads();
-        fwd_main_groups<LOGN, E, GI + 1, FS, LASTDST>(ar, sm, tw, c0, load, out);
+        sync_slice<S::T, (S::T >> (S0 < 16 ? S0 : 16))>();  // blocks of stage S0 (0: the whole row)
+        fwd_main_groups<LOGN, E, GI + 1, FS, LASTDST, PERM>(ar, sm, tw, c0, load, out);
     }
 }
 
 // FS: the input is already in shared memory (split rows) instead of behind `load`.
 // LASTDST: 1 = results in registers (line pairs), 2 = left in shared memory (natural order).
-template <int LOGN, int E, bool FS, int LASTDST = 1, class A, class Load>
+// PERM: which lane-major twiddle region the last group reads (see lane_major_tw).
+template <int LOGN, int E, bool FS, int LASTDST = 1, int PERM = 1, class A, class Load>
 __device__ void forward_core(const A &ar, typename A::V *sm, const typename A::W *__restrict__ tw, int c0, Load load,
                              u64 (&out)[E]) {
     using S = Shape<LOGN, E>;
     static_assert(LOGN >= 6 && LOGN <= 14, "one CTA covers N = 64 .. 16384");
     if constexpr (S::REM) {
-        fwd_group<LOGN, E, S::REM, 0, FS ? 1 : 0, 0>(ar, sm, tw, c0, load, out);
+        fwd_group<LOGN, E, S::REM, 0, FS ? 1 : 0, 0, 0>(ar, sm, tw, c0, load, out);
         __syncthreads();
     }
-    fwd_main_groups<LOGN, E, 0, FS, LASTDST>(ar, sm, tw, c0, load, out);
+    fwd_main_groups<LOGN, E, 0, FS, LASTDST, PERM>(ar, sm, tw, c0, load, out);
 }
 
 // Forward NTT of one row held by one CTA.
@@ -400,16 +463,20 @@ __device__ void forward_split_eo(const A &ar, typename A::V *sm, const typename 
     cg::cluster_group cluster = cg::this_cluster();
     int dummy = 0;
     auto noload = [&](int) { return (u64)dummy; };
-    forward_core<LL, E, true, 2>(ar, sm, tw, 1, noload, out);
+    forward_core<LL, E, true, 2, 2>(ar, sm, tw, 1, noload, out);
     cluster.sync();  // both parity classes are complete
-    const V *pe = cluster.map_shared_rank(sm, 0);
-    const V *po = cluster.map_shared_rank(sm, 1);
+    const V *peer = cluster.map_shared_rank(sm, r ^ 1);
     constexpr int H = (1 << LL) / 2;
     static_assert(H == (E / 2) * S::T, "E/2 pairs per thread");
+    V mine[E / 2], other[E / 2];
+#pragma unroll
+    for (int i = 0; i < E / 2; ++i) other[i] = peer[pad(r * H + (int)threadIdx.x + S::T * i)];
+#pragma unroll
+    for (int i = 0; i < E / 2; ++i) mine[i] = sm[pad(r * H + (int)threadIdx.x + S::T * i)];
 #pragma unroll
     for (int i = 0; i < E / 2; ++i) {
         const int b = r * H + (int)threadIdx.x + S::T * i;
-        V u = pe[pad(b)], v = po[pad(b)];
+        V u = r ? other[i] : mine[i], v = r ? mine[i] : other[i];
         ar.fwd(u, v, __ldg(tw + (1 << LL) + b));
         out[2 * i] = ar.out_fwd(u);
         out[2 * i + 1] = ar.out_fwd(v);
@@ -435,6 +502,11 @@ HD void inv_group(const A &ar, typename A::V *sm, const typename A::W *__restric
         const int ulow = u & ((1 << LB) - 1);
         const int uhigh = u >> LB;
         const int base = (uhigh << (LOGN - S0)) | ulow;
+        // the first inverse group (register input) is the forward's last group mirrored
+        constexpr bool LANE_MAJOR = NTT_TW_LANE_MAJOR && SRC == 1 && LB == 0 && RB == 4 && UPT == 1 && !(LASTS && S0 == 0);
+        int lm_stride = 0;
+        const typename A::W *lm = nullptr;
+        if constexpr (LANE_MAJOR) lm = lane_major_tw<LOGN, S0, 1>(itw, c0, u, lm_stride);
         V x[R];
         if constexpr (SRC == 1) {
             static_assert(UPT == 1 && R == E && LB == 0, "register input needs one radix-E unit per thread");
@@ -461,7 +533,9 @@ HD void inv_group(const A &ar, typename A::V *sm, const typename A::W *__restric
                     ar.inv_last(x[m], x[m + half], last_u, last_v);
                 } else {
                     NTT_ASSERT((c0 << (S0 + q)) + (uhigh << q) + (m >> (RB - q)) < 4 * S::N && uhigh < (1 << S0));
-                    const auto w = __ldg(itw + (c0 << (S0 + q)) + (uhigh << q) + (m >> (RB - q)));
+                    typename A::W w;
+                    if constexpr (LANE_MAJOR) w = __ldg(lm + ((1 << q) - 1 + (m >> (RB - q))) * lm_stride);
+                    else w = __ldg(itw + (c0 << (S0 + q)) + (uhigh << q) + (m >> (RB - q)));
                     ar.inv(x[m], x[m + half], w);
                     if constexpr (A::THROTTLE > 0) {
                         if ((m % A::THROTTLE) == A::THROTTLE - 1) asm volatile("" ::: "memory");
@@ -493,7 +567,8 @@ HD void inv_main_groups(const A &ar, typename A::V *sm, const typename A::W *__r
     inv_group<LOGN, E, S::LOGE, S0, first ? 1 : 0, (last && !NF) ? 1 : 0, !NF>(ar, sm, itw, c0, in, store, last_u,
                                                                             last_v);
     if constexpr (GI > 0) {
-        __syncthreads();
+        // the next group (first stage S0 - LOGE) reads inside blocks of that stage
+        sync_slice<S::T, (S::T >> (S0 - S::LOGE < 16 ? S0 - S::LOGE : 16))>();
         inv_main_groups<LOGN, E, GI - 1, NF>(ar, sm, itw, c0, in, store, last_u, last_v);
     }
 }

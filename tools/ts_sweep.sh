@@ -16,7 +16,7 @@ for k, x in list(d["kernels"].items())[:4]: print("   ", k, x)
 PY
 done
 cat gpurun_out/${T}_sweep.log
-for ts in ${5:-4 99}; do
+for ts in ${5-4 99}; do
   env HEB_MODUP_TS=$ts $X timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct --clock-control none \
       -k "regex:k_ks_modup_fused" -s 4 -c 8 --csv --log-file gpurun_out/${T}_ts${ts}_dram.csv \
       python bench.py --config $C --pipelines 1 --steps 1 --warmup 1 --skip-cpu --skip-cfg1 --skip-u64 --no-prof > gpurun_out/${T}_ts${ts}_ncu.log 2>&1
