@@ -186,14 +186,21 @@ __device__ __forceinline__ void conv_body(u64 *wsm, const Ctx &K, const heb_ct &
 // once per output cell.  Bounds: limbs of the component sums < 2^21, so every term is
 // < 2^42 and a sum of `taps` terms stays below 2^53 for taps <= 256.  The weight limbs
 // and their Karatsuba sums are staged in shared memory as double pairs
-// ([tap][filter][(b0h, b0l), (b1h, b1l), (b0h + b1h, b0l + b1l)][XF]).
+// ([tap][filter][(b0h, b0l), (b1h, b1l), (b0h + b1h, b0l + b1l)][XF]).  The kernel runs
+// the shared-memory pipe at 70% and the DFMA pipe at 50% (ncu r2b); forming the sums in
+// registers instead (CONV_WPAIRS=2: a third fewer 16-byte loads, 2 more DADD per tap and
+// filter) measured 23% SLOWER (r2h: more spills at the 128-register bound), as did two
+// taps of input loads in flight (CONV_AHEAD=2, +4%).
 namespace {
 constexpr int XF = 16;  // positions per CTA
 constexpr int SF = 16;  // workers per position -> 256 threads
 constexpr int FGF = CONV_FGF;  // filters per CTA group
 constexpr int FP_MAX_TAPS = 256;
 constexpr u64 M20 = (1ull << 20) - 1;
-constexpr int WPAIRS = 3;  // staged weight double2 per (tap, filter)
+#ifndef CONV_WPAIRS
+#define CONV_WPAIRS 3
+#endif
+constexpr int WPAIRS = CONV_WPAIRS;  // staged weight double2 per (tap, filter): 3 = with the Karatsuba sums
 }  // namespace
 
 __device__ __forceinline__ void conv_body_limbs(double *wl, const Ctx &K, const heb_ct &A, const heb_ct &B,
@@ -211,7 +218,7 @@ __device__ __forceinline__ void conv_body_limbs(double *wl, const Ctx &K, const 
     __shared__ int64_t toff[FP_MAX_TAPS];
     for (int e = w; e < taps * FGF; e += SF) {
         const int tap = e / FGF, fl = e % FGF;
-        // [tap][filter][pair][XF] double2: (b0h, b0l), (b1h, b1l), (b0h + b1h, b0l + b1l)
+        // [tap][filter][pair][XF] double2: (b0h, b0l), (b1h, b1l) [, (b0h + b1h, b0l + b1l)]
         double2 *dst = reinterpret_cast<double2 *>(wl) + (size_t)(tap * FGF + fl) * WPAIRS * XF + xl;
         if (fl < nf) {
             const u64 *src = B.data + ((int64_t)(f0 + fl) * taps + tap) * B.ct_stride + roff;
@@ -220,9 +227,10 @@ __device__ __forceinline__ void conv_body_limbs(double *wl, const Ctx &K, const 
             const double b1h = ntt::u2d(b1 >> 20), b1l = ntt::u2d(b1 & M20);
             dst[0] = make_double2(b0h, b0l);
             dst[XF] = make_double2(b1h, b1l);
-            dst[2 * XF] = make_double2(b0h + b1h, b0l + b1l);
+            if constexpr (WPAIRS == 3) dst[2 * XF] = make_double2(b0h + b1h, b0l + b1l);
         } else {
-            dst[0] = dst[XF] = dst[2 * XF] = make_double2(0.0, 0.0);
+            dst[0] = dst[XF] = make_double2(0.0, 0.0);
+            if constexpr (WPAIRS == 3) dst[2 * XF] = make_double2(0.0, 0.0);
         }
     }
     for (int tap = threadIdx.x; tap < taps; tap += blockDim.x) {
@@ -278,8 +286,16 @@ __device__ __forceinline__ void conv_body_limbs(double *wl, const Ctx &K, const 
                     for (int fl = 0; fl < FGF; ++fl) {
                         {  // every slot: zero weights past the last filter
                             const double2 w0 = wt[(WPAIRS * fl) * XF], w1 = wt[(WPAIRS * fl + 1) * XF];
-                            const double2 ws = wt[(WPAIRS * fl + 2) * XF];
-                            const double b0h = w0.x, b0l = w0.y, b1h = w1.x, b1l = w1.y, bsh = ws.x, bsl = ws.y;
+                            const double b0h = w0.x, b0l = w0.y, b1h = w1.x, b1l = w1.y;
+                            double bsh, bsl;
+                            if constexpr (WPAIRS == 3) {
+                                const double2 ws = wt[(WPAIRS * fl + 2) * XF];
+                                bsh = ws.x;
+                                bsl = ws.y;
+                            } else {
+                                bsh = b0h + b1h;
+                                bsl = b0l + b1l;
+                            }
                             h0[fl] = fma(a0h, b0h, h0[fl]);
                             q0[fl] = fma(a0h, b0l, fma(a0l, b0h, q0[fl]));
                             l0[fl] = fma(a0l, b0l, l0[fl]);
