@@ -24,8 +24,11 @@ static bool getenv_flag(const char *name) {
 }
 
 namespace {
-constexpr int XC = 32;  // positions per CTA (one warp-width)
-constexpr int SW = 8;   // workers per position  -> 256 threads
+#ifndef CONV_XC
+#define CONV_XC 32
+#endif
+constexpr int XC = CONV_XC;   // positions per CTA (integer-row body)
+constexpr int SW = 256 / XC;  // workers per position  -> 256 threads
 #ifndef CONV_FGF
 #define CONV_FGF 5
 #endif
@@ -192,8 +195,11 @@ __device__ __forceinline__ void conv_body(u64 *wsm, const Ctx &K, const heb_ct &
 // filter) measured 23% SLOWER (r2h: more spills at the 128-register bound), as did two
 // taps of input loads in flight (CONV_AHEAD=2, +4%).
 namespace {
-constexpr int XF = 16;  // positions per CTA
-constexpr int SF = 16;  // workers per position -> 256 threads
+#ifndef CONV_XF
+#define CONV_XF 16
+#endif
+constexpr int XF = CONV_XF;   // positions per CTA
+constexpr int SF = 256 / XF;  // workers per position -> 256 threads
 constexpr int FGF = CONV_FGF;  // filters per CTA group
 constexpr int FP_MAX_TAPS = 256;
 constexpr u64 M20 = (1ull << 20) - 1;
