@@ -444,7 +444,9 @@ static constexpr size_t smem_bytes() {
 
 template <class K>
 static cudaError_t prep_kernel(K kernel, size_t smem) {
-    if (smem > 48 * 1024)
+    // the 48 KB default limit covers static + dynamic shared memory: opt in early enough
+    // that a kernel's static arrays (a few KB) never push a launch over it
+    if (smem > 32 * 1024)
         return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return cudaSuccess;
 }

@@ -24,11 +24,15 @@ static bool getenv_flag(const char *name) {
 }
 
 namespace {
+// Positions per CTA (256 threads = positions x workers, a worker strides over the output
+// cells).  Two widths are compiled: the wide one (512-byte warp accesses) while two CTAs'
+// weight stages fit an SM's shared memory, the narrow one beyond that -- cfg4's second
+// convolution (45 taps) stages 173 KB at the wide width, which leaves ONE 8-warp CTA per
+// SM; at half the width two CTAs are resident (r2h: 78 -> ~52 ms per launch, while the
+// 25-tap convolutions are 25% slower narrow).
 #ifndef CONV_XC
-#define CONV_XC 32
+#define CONV_XC 32  // wide width of the integer-row body (narrow: half)
 #endif
-constexpr int XC = CONV_XC;   // positions per CTA (integer-row body)
-constexpr int SW = 256 / XC;  // workers per position  -> 256 threads
 #ifndef CONV_FGF
 #define CONV_FGF 5
 #endif
@@ -46,11 +50,12 @@ constexpr int FG = CONV_FGF;  // filters per CTA group
 // the split-limb path, FP64 rows with one exact FP64 modular product per term).
 // Output cells [cell_lo, cell_hi) of row r (the integer rows split their cells over
 // several CTAs, see k_conv_tensor).
-template <bool FLUSH, bool ALLOW_FP>
+template <bool FLUSH, bool ALLOW_FP, int XC>
 __device__ __forceinline__ void conv_body(u64 *wsm, const Ctx &K, const heb_ct &A, const heb_ct &B, const heb_ct &D,
                                           int C, int m, int n, int F, int P, int Q, int s, int om, int on, int logn,
                                           int flush, int bx, int r, int cell_lo, int cell_hi) {
     // wsm: [tap][fl][comp][XC]
+    constexpr int SW = 256 / XC;  // workers per position
     const int xl = threadIdx.x % XC, w = threadIdx.x / XC;
     const int x = bx * XC + xl;
     const int f0 = blockIdx.z * FG;
@@ -196,10 +201,8 @@ __device__ __forceinline__ void conv_body(u64 *wsm, const Ctx &K, const heb_ct &
 // taps of input loads in flight (CONV_AHEAD=2, +4%).
 namespace {
 #ifndef CONV_XF
-#define CONV_XF 16
+#define CONV_XF 16  // wide width of the split-limb body (narrow: half)
 #endif
-constexpr int XF = CONV_XF;   // positions per CTA
-constexpr int SF = 256 / XF;  // workers per position -> 256 threads
 constexpr int FGF = CONV_FGF;  // filters per CTA group
 constexpr int FP_MAX_TAPS = 256;
 constexpr u64 M20 = (1ull << 20) - 1;
@@ -209,9 +212,11 @@ constexpr u64 M20 = (1ull << 20) - 1;
 constexpr int WPAIRS = CONV_WPAIRS;  // staged weight double2 per (tap, filter): 3 = with the Karatsuba sums
 }  // namespace
 
+template <int XF>
 __device__ __forceinline__ void conv_body_limbs(double *wl, const Ctx &K, const heb_ct &A, const heb_ct &B,
                                                 const heb_ct &D, int C, int m, int n, int F, int P, int Q, int s,
                                                 int om, int on, int logn, int bx, int r) {
+    constexpr int SF = 256 / XF;  // workers per position
     const int xl = threadIdx.x % XF, w = threadIdx.x / XF;
     const int x = bx * XF + xl;
     const PrimeInfo Pr = K.pi[r];
@@ -346,14 +351,15 @@ struct ConvMap {
     int8_t fp_rows[32], int_rows[32];
 };
 
-template <bool FLUSH, bool LIMBS>
+template <bool FLUSH, bool LIMBS, bool NARROW>
 __global__ void __launch_bounds__(256, CONV_MINB) k_conv_tensor(Ctx K, heb_ct A, heb_ct B, heb_ct D, int C, int m, int n,
                                                          int F, int P, int Q, int s, int om, int on, int logn,
                                                          int flush, ConvMap map) {
     extern __shared__ u64 conv_smem[];
+    constexpr int XC = NARROW ? CONV_XC / 2 : CONV_XC, XF = NARROW ? CONV_XF / 2 : CONV_XF;
     const int cells = om * on;
     if (!LIMBS) {
-        conv_body<FLUSH, true>(conv_smem, K, A, B, D, C, m, n, F, P, Q, s, om, on, logn, flush, blockIdx.x,
+        conv_body<FLUSH, true, XC>(conv_smem, K, A, B, D, C, m, n, F, P, Q, s, om, on, logn, flush, blockIdx.x,
                                blockIdx.y, 0, cells);
         return;
     }
@@ -363,12 +369,12 @@ __global__ void __launch_bounds__(256, CONV_MINB) k_conv_tensor(Ctx K, heb_ct A,
     if (is_int) {
         const int per_row = map.xc_blocks * map.cs;
         const int rem = ib % per_row, split = rem % map.cs;
-        conv_body<FLUSH, false>(conv_smem, K, A, B, D, C, m, n, F, P, Q, s, om, on, logn, flush, rem / map.cs,
+        conv_body<FLUSH, false, XC>(conv_smem, K, A, B, D, C, m, n, F, P, Q, s, om, on, logn, flush, rem / map.cs,
                                 map.int_rows[ib / per_row], (int)((long)split * cells / map.cs),
                                 (int)((long)(split + 1) * cells / map.cs));
     } else {
         const int fb = b - ib;
-        conv_body_limbs(reinterpret_cast<double *>(conv_smem), K, A, B, D, C, m, n, F, P, Q, s, om, on, logn,
+        conv_body_limbs<XF>(reinterpret_cast<double *>(conv_smem), K, A, B, D, C, m, n, F, P, Q, s, om, on, logn,
                         fb % map.xf_blocks, map.fp_rows[fb / map.xf_blocks]);
     }
 }
@@ -376,17 +382,31 @@ __global__ void __launch_bounds__(256, CONV_MINB) k_conv_tensor(Ctx K, heb_ct A,
 extern "C" int heb_conv_tensor(heb_ctx *c, heb_ct a, heb_ct b, heb_ct d, int channels, int m, int n, int filters,
                                int kp, int kq, int stride, int k, void *stream) {
     if (!c || channels < 1 || filters < 1 || kp < 1 || kq < 1 || stride < 1 || kp > m || kq > n || k < 1 ||
-        k > c->num_rows || c->n % XC)
+        k > c->num_rows || c->n % CONV_XC)
         return fail(HEB_EINVAL, "heb_conv_tensor: bad args");
     const int om = (m - kp) / stride + 1, on = (n - kq) / stride + 1;
     const int taps = channels * kp * kq;
-    const size_t sm = sizeof(u64) * (size_t)taps * FG * 2 * XC;
-    if (sm > 220 * 1024) return fail(HEB_EUNSUP, "heb_conv_tensor: %d taps exceed the shared-memory stage", taps);
     cudaStream_t st = (cudaStream_t)stream;
     const bool need_flush = taps > c->flush;
-    const size_t smf = sizeof(double2) * (size_t)taps * FGF * WPAIRS * XF;
-    const bool limbs = taps <= FP_MAX_TAPS && smf <= 200 * 1024 && !getenv_flag("HEB_CONV_NO_LIMBS");
-    const size_t smem = limbs ? std::max(sm, smf) : sm;
+    // shared-memory stage of one CTA at positions-per-CTA (xc, xf): integer body / split-limb body
+    auto stage = [&](int xc, int xf, bool &limbs) {
+        const size_t sm = sizeof(u64) * (size_t)taps * FG * 2 * xc;
+        const size_t smf = sizeof(double2) * (size_t)taps * FGF * WPAIRS * xf;
+        limbs = taps <= FP_MAX_TAPS && smf <= 200 * 1024 && !getenv_flag("HEB_CONV_NO_LIMBS");
+        return limbs ? std::max(sm, smf) : sm;
+    };
+    // wide CTAs while two of them fit an SM (227 KB, 1 KB reserved per CTA plus the static arrays)
+    static const int narrow_env = [] {
+        const char *e = getenv("HEB_CONV_NARROW");  // 0 / 1 force the width (experiments)
+        return e && *e ? atoi(e) : -1;
+    }();
+    bool limbs = false;
+    size_t smem = stage(CONV_XC, CONV_XF, limbs);
+    const bool narrow = narrow_env >= 0 ? narrow_env != 0 : smem > 110 * 1024;
+    const int XC = narrow ? CONV_XC / 2 : CONV_XC, XF = narrow ? CONV_XF / 2 : CONV_XF;
+    if (narrow) smem = stage(XC, XF, limbs);
+    if (sizeof(u64) * (size_t)taps * FG * 2 * XC > 220 * 1024)
+        return fail(HEB_EUNSUP, "heb_conv_tensor: %d taps exceed the shared-memory stage", taps);
     static_assert(FG == FGF, "both bodies use the same filter groups");
     ConvMap map{};
     map.xf_blocks = c->n / XF;
@@ -408,17 +428,20 @@ extern "C" int heb_conv_tensor(heb_ctx *c, heb_ct a, heb_ct b, heb_ct d, int cha
                             : dim3(c->n / XC, k, (filters + FG - 1) / FG);
     const double nout = (double)filters * om * on;
     PROF("k_conv_tensor", st, 8.0 * c->n * k * (2.0 * channels * m * n + 2.0 * filters * taps + 3.0 * nout));
-#define CONV_LAUNCH(FL, LI)                                                                                   \
-    {                                                                                                         \
-        CUDA_TRY(prep_kernel(k_conv_tensor<FL, LI>, smem));                                                   \
-        k_conv_tensor<FL, LI><<<grid, 256, smem, st>>>(kctx(c), a, b, d, channels, m, n, filters, kp, kq, stride, \
-                                                       om, on, c->log_n, c->flush, map);                     \
+#define CONV_LAUNCH(FL, LI, NA)                                                                                   \
+    {                                                                                                             \
+        CUDA_TRY(prep_kernel(k_conv_tensor<FL, LI, NA>, smem));                                                   \
+        k_conv_tensor<FL, LI, NA><<<grid, 256, smem, st>>>(kctx(c), a, b, d, channels, m, n, filters, kp, kq, stride, \
+                                                           om, on, c->log_n, c->flush, map);                     \
     }
+#define CONV_LAUNCH_W(FL, LI) \
+    if (narrow) CONV_LAUNCH(FL, LI, true) else CONV_LAUNCH(FL, LI, false)
     if (limbs) {
-        if (need_flush) CONV_LAUNCH(true, true) else CONV_LAUNCH(false, true)
+        if (need_flush) { CONV_LAUNCH_W(true, true) } else { CONV_LAUNCH_W(false, true) }
     } else {
-        if (need_flush) CONV_LAUNCH(true, false) else CONV_LAUNCH(false, false)
+        if (need_flush) { CONV_LAUNCH_W(true, false) } else { CONV_LAUNCH_W(false, false) }
     }
+#undef CONV_LAUNCH_W
 #undef CONV_LAUNCH
     LAUNCH_CHECK();
     return HEB_OK;
@@ -426,4 +449,4 @@ extern "C" int heb_conv_tensor(heb_ctx *c, heb_ct a, heb_ct b, heb_ct d, int cha
 
 // Largest tap count heb_conv sends to the fused kernel: what its shared-memory stage
 // holds, capped at 64 (beyond that the index-driven heb_dot_tensor measured faster).
-int conv_tensor_max_taps() { return std::min(64, (int)(220 * 1024 / (sizeof(u64) * FG * 2 * XC))); }
+int conv_tensor_max_taps() { return std::min(64, (int)(220 * 1024 / (sizeof(u64) * FG * 2 * (CONV_XC / 2)))); }

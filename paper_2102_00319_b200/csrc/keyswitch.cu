@@ -444,6 +444,18 @@ struct TargetList {
 #ifndef MODUP_STAGE_SPLIT
 #define MODUP_STAGE_SPLIT 0
 #endif
+// parity-split rows: cross-CTA stage fed by st.async pushes (ntt::forward_split_eo_push)
+// instead of remote loads between two cluster barriers
+#ifndef MODUP_PUSH
+#define MODUP_PUSH 0
+#endif
+// dynamic shared memory of the fused ModUp: the transform buffer, plus the receive region
+// of the push exchange for parity-split rows
+template <int LOGN>
+static constexpr size_t modup_smem_bytes() {
+    return smem_bytes<LOGN>() +
+           (Row<LOGN>::SP == 2 && MODUP_EO && MODUP_PUSH ? sizeof(u64) * ntt::xchg::recv_words<Row<LOGN>::LL, 16>() : 0);
+}
 #ifndef MODUP_KEY_PREFETCH
 #define MODUP_KEY_PREFETCH 0
 #endif
@@ -490,6 +502,8 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
         bool first = true;
         int staged_for = -1;  // digit whose row (this CTA's part) sits in shared memory
         constexpr bool EO = DIGITS_EO<LOGN> && ENG != 0;  // parity-split rows, staged digits
+        constexpr bool PUSH = EO && MODUP_PUSH;
+        int seq = 0;  // exchanges done (push protocol)
         if constexpr (EO || (Row<LOGN>::SPLIT && MODUP_STAGE_SPLIT && ENG != 0)) {
             // split rows only ever transform from staged digits: stage the first one now
             const int j0 = t == 0 ? 1 : 0;
@@ -498,6 +512,7 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
                 staged_for = j0;
             }
         }
+        if constexpr (PUSH) ntt::xchg::init();
         for (int j = 0; j < k; ++j) {
             if (MODUP_KEY_PREFETCH && ENG != 0 && threadIdx.x == 0)
                 prefetch_key<LOGN, ENG == 1>(key + (((size_t)j * R + gt) * 2) * n);
@@ -529,7 +544,8 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
                                     s2[q] = ntt::u2d(ld.conv(reinterpret_cast<const i64 *>(sm)[q]));
                                 });
                             }
-                            ntt::forward_split_eo<LL, 16>(ar, s2, tw, y, rpart<LOGN>());
+                            if constexpr (PUSH) ntt::forward_split_eo_push<LL, 16>(ar, s2, tw, y, rpart<LOGN>(), seq++);
+                            else ntt::forward_split_eo<LL, 16>(ar, s2, tw, y, rpart<LOGN>());
                         } else if constexpr (Row<LOGN>::SPLIT) {
                             if constexpr (MODUP_STAGE_SPLIT) ntt::forward_split_staged<LL, 16, Row<LOGN>::SP>(ar, s2, tw, ld, y, rpart<LOGN>());
                             else ntt::forward_split<LL, 16, Row<LOGN>::SP>(ar, s2, tw, ld, y, rpart<LOGN>());
@@ -555,7 +571,8 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
                                 const int q = ntt::pad(i);
                                 sm[q] = ld.conv(reinterpret_cast<const i64 *>(sm)[q]);
                             });
-                            ntt::forward_split_eo<LL, 16>(ar, sm, tw, y, rpart<LOGN>());
+                            if constexpr (PUSH) ntt::forward_split_eo_push<LL, 16>(ar, sm, tw, y, rpart<LOGN>(), seq++);
+                            else ntt::forward_split_eo<LL, 16>(ar, sm, tw, y, rpart<LOGN>());
                         } else if constexpr (Row<LOGN>::SPLIT) {
                             if constexpr (MODUP_STAGE_SPLIT) ntt::forward_split_staged<LL, 16, Row<LOGN>::SP>(ar, sm, tw, ld, y, rpart<LOGN>());
                             else ntt::forward_split<LL, 16, Row<LOGN>::SP>(ar, sm, tw, ld, y, rpart<LOGN>());
@@ -601,6 +618,7 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
             modup_store<LOGN, true>(ta, o0, o1, pos, P);
         else
             modup_store<LOGN, false>(ta, o0, o1, pos, P);
+        if constexpr (PUSH) ntt::xchg::fini();
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -938,9 +956,10 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
     constexpr size_t sm = smem_bytes<LOGN>();
     PREP_ENGINES(k_ks_head, sm);
     CUDA_TRY(prep_kernel(k_ks_modup_ntt<LOGN>, sm));
+    constexpr size_t smu = modup_smem_bytes<LOGN>();
     CUDA_TRY(prep_kernel(k_ks_modup_fused<LOGN, 0>, sm));
-    CUDA_TRY(prep_kernel(k_ks_modup_fused<LOGN, 1>, sm));
-    CUDA_TRY(prep_kernel(k_ks_modup_fused<LOGN, 2>, sm));
+    CUDA_TRY(prep_kernel(k_ks_modup_fused<LOGN, 1>, smu));
+    CUDA_TRY(prep_kernel(k_ks_modup_fused<LOGN, 2>, smu));
     PREP_ENGINES(k_ks_down_head, sm);
     PREP_ENGINES(k_ks_down_head_cl, sm);
     PREP_ENGINES(k_ks_down_rescale_tail, sm);
@@ -1017,10 +1036,10 @@ static int launch_keyswitch(heb_ctx *c, heb_ct src, int comp, const ulonglong2 *
                 cudaStream_t ist = st;
                 if (concurrent && tl_int.n) CUDA_TRY(side_fork(c, st, &ist));
                 if (tl_int.n)
-                    CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 2>, mgrid(tl_int), KT<LOGN>, sm, ist, K,
+                    CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 2>, mgrid(tl_int), KT<LOGN>, smu, ist, K,
                                                s, comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt, tl_int, mts(tl_int)));
                 if (tl_fp.n)
-                    CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 1>, mgrid(tl_fp), KT<LOGN>, sm, st, K,
+                    CUDA_TRY(launch_rows<LOGN>(k_ks_modup_fused<LOGN, 1>, mgrid(tl_fp), KT<LOGN>, smu, st, K,
                                                s, comp, (const i64 *)sD.p, key, k, (u64 *)sA.p, cnt, tl_fp, mts(tl_fp)));
                 if (concurrent && tl_int.n) CUDA_TRY(side_join(c, st));
             } else {

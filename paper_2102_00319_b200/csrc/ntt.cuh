@@ -227,10 +227,63 @@ HD void sync_slice() {
     }
 }
 
+// Cluster barrier halves for exchanges through (distributed) shared memory.
+// cg::cluster_group::sync() compiles to MEMBAR.ALL.GPU + ERRBAR + CGAERRBAR before the
+// arrive (release at cluster scope: every outstanding global access of the thread is
+// waited for, 4% of the fused ModUp's stall samples at cfg4, ncu r2g) -- not needed when
+// the only data handed over sits in this CTA's shared memory: a CTA barrier has performed
+// the CTA's shared-memory writes, and the peer's loads reach this SM after the cluster
+// barrier completes.  PUBLISH: this CTA wrote shared memory its peers will read.
+#ifndef NTT_RELAXED_CLUSTER_SYNC
+#define NTT_RELAXED_CLUSTER_SYNC 1
+#endif
+template <bool PUBLISH>
+__device__ __forceinline__ void cluster_arrive_smem() {
+#if NTT_RELAXED_CLUSTER_SYNC
+    if constexpr (PUBLISH) __syncthreads();
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+#else
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void cluster_wait() {
+#if NTT_RELAXED_CLUSTER_SYNC
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+#else
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ unsigned long long word_bits(double v) { return (unsigned long long)__double_as_longlong(v); }
+__device__ __forceinline__ unsigned long long word_bits(u64 v) { return v; }
+// "This thread is done reading its peers' shared memory": the arrive must not be issued
+// while a (remote) load is still in flight -- the peer may overwrite the location as soon
+// as the barrier completes -- so it follows a shared-memory store whose data depends on
+// every loaded word (the store cannot issue before the loads have returned); it goes to
+// a scratch word per lane that nothing reads.
+__device__ __forceinline__ unsigned ntt_scratch_addr() {
+    __shared__ unsigned scratch[32];
+    return (unsigned)__cvta_generic_to_shared(&scratch[threadIdx.x & 31]);
+}
+template <class V, int NA, int NB>
+__device__ __forceinline__ void cluster_arrive_after_loads(V *sm, const V (&a)[NA], const V (&b)[NB]) {
+#if NTT_RELAXED_CLUSTER_SYNC
+    unsigned long long acc = 0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) acc |= word_bits(a[i]);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) acc |= word_bits(b[i]);
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(ntt_scratch_addr()), "r"((unsigned)(acc >> 32) | (unsigned)acc) : "memory");
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+#else
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+#endif
+}
+
 // ---------------------------------------------------------------- forward ----
 // One forward group: radix 2^RB covering stages S0 .. S0+RB-1.
 // SRC: 0 = functor load, 1 = shared memory.  DST: 0 = shared memory, 1 = registers (line
-// pairs), 2 = shared memory in place, natural order, for the last group (LB = 0).
+// pairs), 2 = shared memory in place, natural order, for the last group (LB = 0), 3 = raw
+// values of the unit's own positions in registers (last group).
 template <int LOGN, int E, int RB, int S0, int SRC, int DST, int PERM, class A, class Load>
 HD void fwd_group(const A &ar, typename A::V *sm, const typename A::W *__restrict__ tw, int c0, Load &load,
                   u64 (&out)[E]) {
@@ -285,6 +338,11 @@ HD void fwd_group(const A &ar, typename A::V *sm, const typename A::W *__restric
                 NTT_ASSERT(lpos(tid, m, S::T) < S::N && tid < S::T);
                 out[m] = ar.out_fwd(sm[pad(lpos(tid, m, S::T))]);
             }
+        } else if constexpr (DST == 3) {
+            static_assert(UPT == 1 && R == E && LB == 0, "register output needs one radix-E unit per thread");
+            // raw results of this unit's own positions base + m (natural order), no exchange
+#pragma unroll
+            for (int m = 0; m < R; ++m) out[m] = word_bits(x[m]);
         } else if constexpr (DST == 2) {
             static_assert(LB == 0, "in-place output is for the last group");
 #pragma unroll
@@ -459,29 +517,144 @@ __device__ void forward_split_eo(const A &ar, typename A::V *sm, const typename 
                                  int r) {
     using S = Shape<LL, E>;
     using V = typename A::V;
+    using W = typename A::W;
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     int dummy = 0;
     auto noload = [&](int) { return (u64)dummy; };
     forward_core<LL, E, true, 2, 2>(ar, sm, tw, 1, noload, out);
-    cluster.sync();  // both parity classes are complete
+    cluster_arrive_smem<true>();  // this CTA's parity class is complete
     const V *peer = cluster.map_shared_rank(sm, r ^ 1);
     constexpr int H = (1 << LL) / 2;
     static_assert(H == (E / 2) * S::T, "E/2 pairs per thread");
     V mine[E / 2], other[E / 2];
-#pragma unroll
-    for (int i = 0; i < E / 2; ++i) other[i] = peer[pad(r * H + (int)threadIdx.x + S::T * i)];
+    W w[E / 2];
+    // the local halves of the pairs and the last stage's twiddles do not need the peer
 #pragma unroll
     for (int i = 0; i < E / 2; ++i) mine[i] = sm[pad(r * H + (int)threadIdx.x + S::T * i)];
 #pragma unroll
+    for (int i = 0; i < E / 2; ++i) w[i] = __ldg(tw + (1 << LL) + r * H + (int)threadIdx.x + S::T * i);
+    cluster_wait();  // ... and so is the peer's
+#pragma unroll
+    for (int i = 0; i < E / 2; ++i) other[i] = peer[pad(r * H + (int)threadIdx.x + S::T * i)];
+    // both operands have arrived before the peer is told it may reuse its shared memory
+    cluster_arrive_after_loads(sm, other, mine);
+#pragma unroll
     for (int i = 0; i < E / 2; ++i) {
-        const int b = r * H + (int)threadIdx.x + S::T * i;
         V u = r ? other[i] : mine[i], v = r ? mine[i] : other[i];
-        ar.fwd(u, v, __ldg(tw + (1 << LL) + b));
+        ar.fwd(u, v, w[i]);
         out[2 * i] = ar.out_fwd(u);
         out[2 * i + 1] = ar.out_fwd(v);
     }
-    cluster.sync();  // the peer has read this CTA's results: shared memory may be reused
+    cluster_wait();  // the peer has read this CTA's results: shared memory may be reused
+}
+
+// The same transform with the cross-CTA stage fed by PUSHES instead of remote loads
+// (NTT_PUSH_XCHG).  After the last local group every thread holds the 16 results of its
+// own unit (local indices 16 t .. 16 t + 15) in registers.  The CTA that finishes a pair
+// range needs both parity classes of it: results of this CTA's own range stay in place,
+// results of the peer's range are sent to the peer's receive region (behind the
+// transform buffer) with st.async, which counts the bytes on the receiver's mbarrier as
+// they land.  Against forward_split_eo (remote loads between two cluster barriers: 16%
+// of the FP64 launch in the exchange plus 6% in MEMBAR / ERRBAR / UCGABAR, ncu r2g): no
+// cluster barrier and no fence in the loop, no load latency over the SM-to-SM network
+// (the stores are fire-and-forget and start as each warp finishes its group), no L1
+// invalidation (barrier.cluster.wait carries a CCTL.IVALL, which drops the twiddles).
+// Protocol per exchange #seq (both CTAs run the same sequence):
+//   full  (receiver's): 1 arrival (its thread 0, arrive.expect_tx of 2^LL / 2 words)
+//                       + the bytes pushed by the peer; waited with parity seq & 1;
+//   free  (sender's):   1 arrival per exchange, made remotely by the receiver once all
+//                       its threads have read the receive region; a sender waits for
+//                       exchange seq - 1's before it pushes again.
+namespace xchg {
+__device__ __forceinline__ uint32_t bar_addr(int which) {
+    __shared__ __align__(8) unsigned long long bars[2];
+    return (uint32_t)__cvta_generic_to_shared(&bars[which]);
+}
+__device__ __forceinline__ uint32_t peer_addr(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void wait_parity(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n XW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @p bra XD;\n bra XW;\n XD:\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+// Once per CTA before the first exchange: the barriers exist cluster-wide before anything
+// is sent to them.
+__device__ __forceinline__ void init() {
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_addr(0)) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_addr(1)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Before the CTA exits: the peer's last (remote) arrival on this CTA's barrier has landed.
+__device__ __forceinline__ void fini() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <int LL, int E>
+constexpr size_t recv_words() {
+    return (size_t)((1 << LL) / 2 + (1 << LL) / 32);
+}
+}  // namespace xchg
+
+template <int LL, int E = 16, class A>
+__device__ void forward_split_eo_push(const A &ar, typename A::V *sm, const typename A::W *__restrict__ tw,
+                                      u64 (&out)[E], int r, int seq) {
+    using S = Shape<LL, E>;
+    using V = typename A::V;
+    using W = typename A::W;
+    static_assert(E == 16 && sizeof(V) == 8, "16 eight-byte results per thread");
+    constexpr int H = (1 << LL) / 2;
+    static_assert(H == (E / 2) * S::T, "E/2 pairs per thread");
+    V *recv = sm + S::SMEM_WORDS;
+    int dummy = 0;
+    auto noload = [&](int) { return (u64)dummy; };
+    forward_core<LL, E, true, 3, 2>(ar, sm, tw, 1, noload, out);
+    const int base = E * (int)threadIdx.x;  // this thread's unit: local indices base .. base + 15
+    const uint32_t full = xchg::bar_addr(0), fre = xchg::bar_addr(1);
+    if (threadIdx.x == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full), "r"((uint32_t)(H * 8)) : "memory");
+    if ((base >= H) == (r != 0)) {  // warp-uniform: this CTA finishes these pairs itself
+#pragma unroll
+        for (int m = 0; m < E; ++m) reinterpret_cast<u64 *>(sm)[pad(base + m)] = out[m];
+    } else {
+        if (seq > 0) xchg::wait_parity(fre, (uint32_t)((seq - 1) & 1));  // the peer has read the previous push
+        const uint32_t pfull = xchg::peer_addr(full, (uint32_t)(r ^ 1));
+        const uint32_t precv = xchg::peer_addr((uint32_t)__cvta_generic_to_shared(recv), (uint32_t)(r ^ 1));
+        const int idx = base - (r ? 0 : H);  // index inside the peer's pair range
+        const uint32_t dst = precv + 8u * (uint32_t)pad(idx);  // pad(idx + m) = pad(idx) + m for m < 16
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+            asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(dst + 8u * m),
+                         "l"(out[m]), "r"(pfull)
+                         : "memory");
+    }
+    __syncthreads();  // the in-place results are visible to the whole CTA
+    V mine[E / 2], other[E / 2];
+    W w[E / 2];
+#pragma unroll
+    for (int i = 0; i < E / 2; ++i) mine[i] = sm[pad(r * H + (int)threadIdx.x + S::T * i)];
+#pragma unroll
+    for (int i = 0; i < E / 2; ++i) w[i] = __ldg(tw + (1 << LL) + r * H + (int)threadIdx.x + S::T * i);
+    xchg::wait_parity(full, (uint32_t)(seq & 1));  // the peer's half of every pair has landed
+#pragma unroll
+    for (int i = 0; i < E / 2; ++i) other[i] = recv[pad((int)threadIdx.x + S::T * i)];
+#pragma unroll
+    for (int i = 0; i < E / 2; ++i) {
+        V u = r ? other[i] : mine[i], v = r ? mine[i] : other[i];
+        ar.fwd(u, v, w[i]);
+        out[2 * i] = ar.out_fwd(u);
+        out[2 * i + 1] = ar.out_fwd(v);
+    }
+    __syncthreads();  // every thread has read the buffer and the receive region: both may be reused
+    if (threadIdx.x == 0)
+        asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(xchg::peer_addr(fre, (uint32_t)(r ^ 1)))
+                     : "memory");
 }
 
 // ---------------------------------------------------------------- inverse ----
@@ -626,7 +799,8 @@ __device__ void inverse_split(const A &ar, typename A::V *sm, const typename A::
     cg::cluster_group cluster = cg::this_cluster();
     __syncthreads();
     inverse_core<LL, E, true>(ar, sm, itw, SP + r, in, store, last_u, last_v);
-    cluster.sync();
+    cluster_arrive_smem<true>();  // this part's local stages are in shared memory
+    cluster_wait();
     const V *parts[SP];
 #pragma unroll
     for (int q = 0; q < SP; ++q) parts[q] = cluster.map_shared_rank(sm, q);
@@ -641,7 +815,11 @@ __device__ void inverse_split(const A &ar, typename A::V *sm, const typename A::
 #pragma unroll
         for (int q = 0; q < SP; ++q) store((q << LL) + j, ar.out_inv(x[q]));
     }
-    cluster.sync();  // the peers must not reuse their shared memory while it is being read
+    // The peers must not reuse their shared memory while it is being read.  Every loaded
+    // word has been consumed by a store issued above (memory operations do not move across
+    // the arrive), so no load of this thread is still in flight here.
+    cluster_arrive_smem<false>();
+    cluster_wait();
 }
 
 }  // namespace ntt
