@@ -271,14 +271,46 @@ __device__ __forceinline__ ulonglong2 ld_key(const ulonglong2 *p) {
 #ifndef MODUP_KEY_AHEAD_INT
 #define MODUP_KEY_AHEAD_INT 0  // 64 bytes of key per step: more spills than the load-ahead saves
 #endif
-template <int LOGN, bool FP, bool RAW = false>
-__device__ __forceinline__ void modup_acc(uint32_t ta, const u64 (&y)[16], const ulonglong2 *keyrow, int pos,
-                                          bool first, const PrimeInfo &P) {
+template <bool FP>
+struct ModupKey {
+    using KV = typename std::conditional<FP, double2, ulonglong2>::type;
+    static constexpr int NK = FP ? 2 : 4;  // 16-byte key words per step (two position pairs)
+};
+// key words of accumulation step `it` (q = it >> 1: position pairs 2q, 2q + 1; c = it & 1)
+template <int LOGN, bool FP>
+__device__ __forceinline__ void modup_key_step(const ulonglong2 *keyrow, int pos, int it,
+                                               typename ModupKey<FP>::KV (&kv)[ModupKey<FP>::NK]) {
     const int n = 1 << LOGN;
     constexpr int T = KT<LOGN>;
-    using KV = typename std::conditional<FP, double2, ulonglong2>::type;
-    constexpr int NK = FP ? 2 : 4;  // 16-byte key words per step (two position pairs)
+    const int q = it >> 1, c = it & 1;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int off = pos + 2 * T * (2 * q + h);
+        if constexpr (FP) {
+            const double *kd = reinterpret_cast<const double *>(keyrow) + (size_t)c * n;
+            kv[h] = ld_key(reinterpret_cast<const double2 *>(kd + off));
+        } else {
+            const ulonglong2 *kp = keyrow + (size_t)c * n + off;
+            kv[2 * h] = ld_key(kp);
+            kv[2 * h + 1] = ld_key(kp + 1);
+        }
+    }
+}
+// PRE: the key words of step 0 were loaded by the caller (`pre`), e.g. before a barrier wait
+template <int LOGN, bool FP, bool RAW = false, bool PRE = false>
+__device__ __forceinline__ void modup_acc(uint32_t ta, const u64 (&y)[16], const ulonglong2 *keyrow, int pos,
+                                          bool first, const PrimeInfo &P,
+                                          const typename ModupKey<FP>::KV (&pre)[ModupKey<FP>::NK]) {
+    const int n = 1 << LOGN;
+    constexpr int T = KT<LOGN>;
+    using KV = typename ModupKey<FP>::KV;
+    constexpr int NK = ModupKey<FP>::NK;
     auto load_step = [&](int it, KV (&kv)[NK]) {
+        if (PRE && it == 0) {
+#pragma unroll
+            for (int x = 0; x < NK; ++x) kv[x] = pre[x];
+            return;
+        }
         const int q = it >> 1, c = it & 1;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -337,6 +369,13 @@ __device__ __forceinline__ void modup_acc(uint32_t ta, const u64 (&y)[16], const
         tmem_st8(ta + 32 * c + 8 * q, w);
     }
     tmem_wait_st();
+}
+
+template <int LOGN, bool FP, bool RAW = false>
+__device__ __forceinline__ void modup_acc(uint32_t ta, const u64 (&y)[16], const ulonglong2 *keyrow, int pos,
+                                          bool first, const PrimeInfo &P) {
+    typename ModupKey<FP>::KV none[ModupKey<FP>::NK] = {};
+    modup_acc<LOGN, FP, RAW, false>(ta, y, keyrow, pos, first, P, none);
 }
 
 template <int LOGN, bool FP>
@@ -444,6 +483,14 @@ struct TargetList {
 #ifndef MODUP_STAGE_SPLIT
 #define MODUP_STAGE_SPLIT 0
 #endif
+// parity-split rows: the first accumulation step's key words are loaded right after the
+// cross-CTA stage, before the closing cluster-barrier wait and the staging of the next
+// digit, so their L2 latency is covered by both (1 = FP64 targets, 2 = integer targets too).
+// Measured r2h (cfg4, fused ModUp ms per 4 steps): off 1394, FP64 targets 1408, both 1440 --
+// the 8 / 16 registers held across the barrier cost more spills than the latency saves: off.
+#ifndef MODUP_KEY_HOOK
+#define MODUP_KEY_HOOK 0
+#endif
 // parity-split rows: cross-CTA stage fed by st.async pushes (ntt::forward_split_eo_push)
 // instead of remote loads between two cluster barriers
 #ifndef MODUP_PUSH
@@ -517,6 +564,9 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
             if (MODUP_KEY_PREFETCH && ENG != 0 && threadIdx.x == 0)
                 prefetch_key<LOGN, ENG == 1>(key + (((size_t)j * R + gt) * 2) * n);
             u64 y[16];
+            const ulonglong2 *keyrow = key + (((size_t)j * R + gt) * 2) * n;
+            constexpr bool HOOK = EO && !PUSH && (ENG == 1 ? MODUP_KEY_HOOK >= 1 : MODUP_KEY_HOOK >= 2);
+            typename ModupKey<ENG == 1>::KV pre[ModupKey<ENG == 1>::NK];
             if (j == t) {
                 load16<LOGN>(at(src, b, comp, t, LOGN) + pos, y);  // d2_t: congruent digit, no transform
                 if constexpr (ENG == 1) {  // canonical residues -> the raw doubles FpArithRaw hands out
@@ -544,7 +594,9 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
                                     s2[q] = ntt::u2d(ld.conv(reinterpret_cast<const i64 *>(sm)[q]));
                                 });
                             }
-                            if constexpr (PUSH) ntt::forward_split_eo_push<LL, 16>(ar, s2, tw, y, rpart<LOGN>(), seq++);
+                            if constexpr (PUSH && MODUP_PUSH == 2) ntt::forward_split_eo_bulk<LL, 16>(ar, s2, tw, y, rpart<LOGN>(), seq++);
+                            else if constexpr (PUSH) ntt::forward_split_eo_push<LL, 16>(ar, s2, tw, y, rpart<LOGN>(), seq++);
+                            else if constexpr (HOOK) ntt::forward_split_eo<LL, 16>(ar, s2, tw, y, rpart<LOGN>(), [&] { modup_key_step<LOGN, true>(keyrow, pos, 0, pre); });
                             else ntt::forward_split_eo<LL, 16>(ar, s2, tw, y, rpart<LOGN>());
                         } else if constexpr (Row<LOGN>::SPLIT) {
                             if constexpr (MODUP_STAGE_SPLIT) ntt::forward_split_staged<LL, 16, Row<LOGN>::SP>(ar, s2, tw, ld, y, rpart<LOGN>());
@@ -571,7 +623,9 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
                                 const int q = ntt::pad(i);
                                 sm[q] = ld.conv(reinterpret_cast<const i64 *>(sm)[q]);
                             });
-                            if constexpr (PUSH) ntt::forward_split_eo_push<LL, 16>(ar, sm, tw, y, rpart<LOGN>(), seq++);
+                            if constexpr (PUSH && MODUP_PUSH == 2) ntt::forward_split_eo_bulk<LL, 16>(ar, sm, tw, y, rpart<LOGN>(), seq++);
+                            else if constexpr (PUSH) ntt::forward_split_eo_push<LL, 16>(ar, sm, tw, y, rpart<LOGN>(), seq++);
+                            else if constexpr (HOOK) ntt::forward_split_eo<LL, 16>(ar, sm, tw, y, rpart<LOGN>(), [&] { modup_key_step<LOGN, false>(keyrow, pos, 0, pre); });
                             else ntt::forward_split_eo<LL, 16>(ar, sm, tw, y, rpart<LOGN>());
                         } else if constexpr (Row<LOGN>::SPLIT) {
                             if constexpr (MODUP_STAGE_SPLIT) ntt::forward_split_staged<LL, 16, Row<LOGN>::SP>(ar, sm, tw, ld, y, rpart<LOGN>());
@@ -603,8 +657,10 @@ __global__ void __launch_bounds__(KT<LOGN>, ENG == 2 ? MODUP_INT_MINB(LOGN) : MO
                     }
                 }
             }
-            const ulonglong2 *keyrow = key + (((size_t)j * R + gt) * 2) * n;
-            if (ENG == 1)
+            if constexpr (HOOK) {
+                if (j != t) modup_acc<LOGN, ENG == 1, ENG == 1, true>(ta, y, keyrow, pos, first, P, pre);
+                else modup_acc<LOGN, ENG == 1, ENG == 1>(ta, y, keyrow, pos, first, P);
+            } else if (ENG == 1)
                 modup_acc<LOGN, true, true>(ta, y, keyrow, pos, first, P);
             else if (ENG == 0 && HEB_FPSEL(P.use_fp))
                 modup_acc<LOGN, true>(ta, y, keyrow, pos, first, P);

@@ -13,4 +13,4 @@ class A:
     pipelines = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 
 
-print(json.dumps(bench.cfg1_mulrelin(A(), 0)))
+print(json.dumps(bench.cfg1_ops(A(), 0)))
