@@ -192,13 +192,13 @@ __device__ __forceinline__ void conv_body(u64 *wsm, const Ctx &K, const heb_ct &
 // (hh, the two cross terms into one accumulator, ll) instead of a 6-op exact FP64
 // modular product plus an add; the three partial sums of each component are reduced
 // once per output cell.  Bounds: limbs of the component sums < 2^21, so every term is
-// < 2^42 and a sum of `taps` terms stays below 2^53 for taps <= 256.  The weight limbs
+// < 2^42 and a sum of `taps` terms stays below 2^53 for taps <= 256 (schoolbook middle,
+// CONV_SCHOOL: up to four terms < 2^40 per tap into one accumulator, < 2^50).  The weight limbs
 // and their Karatsuba sums are staged in shared memory as double pairs
-// ([tap][filter][(b0h, b0l), (b1h, b1l), (b0h + b1h, b0l + b1l)][XF]).  The kernel runs
-// the shared-memory pipe at 70% and the DFMA pipe at 50% (ncu r2b); forming the sums in
-// registers instead (CONV_WPAIRS=2: a third fewer 16-byte loads, 2 more DADD per tap and
-// filter) measured 23% SLOWER (r2h: more spills at the 128-register bound), as did two
-// taps of input loads in flight (CONV_AHEAD=2, +4%).
+// ([tap][filter][(b0h, b0l), (b1h, b1l) [, (b0h + b1h, b0l + b1l)]][XF]).  Forming the
+// Karatsuba sums in registers instead of staging them (CONV_WPAIRS=2 with the Karatsuba
+// middle: 2 more DADD per tap and filter) measured 23% SLOWER (more spills at the
+// 128-register bound), as did two taps of input loads in flight (CONV_AHEAD=2, +4%).
 namespace {
 #ifndef CONV_XF
 #define CONV_XF 16  // wide width of the split-limb body (narrow: half)
@@ -206,8 +206,18 @@ namespace {
 constexpr int FGF = CONV_FGF;  // filters per CTA group
 constexpr int FP_MAX_TAPS = 256;
 constexpr u64 M20 = (1ull << 20) - 1;
+// CONV_SCHOOL: the middle component as a0 b1 + a1 b0 (8 DFMA per tap and filter) instead of
+// the Karatsuba product of the sums (4 DFMA + a third staged pair).  The kernel is bound by
+// the shared-memory data pipe, not the DFMA pipe (ncu r2h: a warp-wide 16-byte load costs
+// ~3.6 wavefronts whatever the lanes share, 79% of the LSU data pipe at 39% FP64): two
+// staged pairs per (tap, filter) instead of three trade a third of that traffic for a
+// third more DFMA, with fewer live registers.  Measured r2h (cfg4, ms per conv launch):
+// Karatsuba middle 37.55, this 36.32; cfg2 unchanged (1.86 / 1.87).
+#ifndef CONV_SCHOOL
+#define CONV_SCHOOL 1
+#endif
 #ifndef CONV_WPAIRS
-#define CONV_WPAIRS 3
+#define CONV_WPAIRS (CONV_SCHOOL ? 2 : 3)
 #endif
 constexpr int WPAIRS = CONV_WPAIRS;  // staged weight double2 per (tap, filter): 3 = with the Karatsuba sums
 }  // namespace
@@ -313,9 +323,17 @@ __device__ __forceinline__ void conv_body_limbs(double *wl, const Ctx &K, const 
                             h2[fl] = fma(a1h, b1h, h2[fl]);
                             q2[fl] = fma(a1h, b1l, fma(a1l, b1h, q2[fl]));
                             l2[fl] = fma(a1l, b1l, l2[fl]);
+#if CONV_SCHOOL
+                            (void)bsh;
+                            (void)bsl;
+                            h1[fl] = fma(a0h, b1h, fma(a1h, b0h, h1[fl]));
+                            q1[fl] = fma(a0h, b1l, fma(a0l, b1h, fma(a1h, b0l, fma(a1l, b0h, q1[fl]))));
+                            l1[fl] = fma(a0l, b1l, fma(a1l, b0l, l1[fl]));
+#else
                             h1[fl] = fma(ash, bsh, h1[fl]);
                             q1[fl] = fma(ash, bsl, fma(asl, bsh, q1[fl]));
                             l1[fl] = fma(asl, bsl, l1[fl]);
+#endif
                         }
                     }
                 }
@@ -330,7 +348,7 @@ __device__ __forceinline__ void conv_body_limbs(double *wl, const Ctx &K, const 
             if (fl < nf) {
                 const double e0 = comb(h0[fl], q0[fl], l0[fl]);
                 const double e2 = comb(h2[fl], q2[fl], l2[fl]);
-                const double e1 = comb(h1[fl], q1[fl], l1[fl]) - e0 - e2;
+                const double e1 = CONV_SCHOOL ? comb(h1[fl], q1[fl], l1[fl]) : comb(h1[fl], q1[fl], l1[fl]) - e0 - e2;
                 u64 *dp = D.data + ((int64_t)(f0 + fl) * cells + cell) * D.ct_stride + roff;
                 dp[0] = ntt::fcanon(e0, pd, pinvd);
                 dp[D.comp_stride] = ntt::fcanon(e1, pd, pinvd);
