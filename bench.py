@@ -290,7 +290,8 @@ def run_gpu(args) -> None:
         e2e_u64 = {"value": round(e2e_measure(x_host, None), 3), "unit": UNIT,
                    "h2d_bytes_per_step": int(x_host.numel() * 8),
                    "d2h_bytes_per_step": int(out_count * 2 * out_k * be.n * 8),
-                   "wire_format": "u64 words per residue (the reference's CkksCipher payload layout)"}
+                   "wire_format": "u64 words per residue (the reference's CkksCipher payload layout), copied into a "
+                                  "device staging buffer and moved into the step's input buffer by one device copy"}
         del x_host
         ev.drop_input_buffers()
 

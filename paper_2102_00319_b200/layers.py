@@ -472,6 +472,11 @@ class LayerEvaluator:
         ``unpacked_shape``: the host inputs are in the bit-packed wire format
         (``B200Backend.pack_batch``) of batches of this (B, 2, K, N) shape; they are
         unpacked on the device, and the next copy of a pipeline overlaps its compute.
+        Unpacked (u64 payload) inputs also land in a per-pipeline staging buffer and are
+        moved into the graph's input buffer by a device copy, so that a pipeline's next
+        host->device copy does not wait for its whole evaluation (the captured graph reads
+        its input buffer until the first layer is done); without room for the staging
+        buffer the copy goes straight into the input buffer as before.
         """
         caller = torch.cuda.current_stream(self.be.dev)
         P = max(1, pipelines)
@@ -487,6 +492,18 @@ class LayerEvaluator:
                     self._inbufs[key] = torch.empty(tuple(host_inputs[0].shape), dtype=host_inputs[0].dtype,
                                                     device=self.be.dev)
                 stage[p] = self._inbufs[key]
+        else:
+            try:
+                for p in range(P):
+                    key = (("staged",) + shape, p)
+                    if key not in self._inbufs:
+                        self._inbufs[key] = torch.empty(shape, dtype=host_inputs[0].dtype, device=self.be.dev)
+                    stage[p] = self._inbufs[key]
+            except torch.cuda.OutOfMemoryError:
+                for p in range(P):
+                    self._inbufs.pop((("staged",) + shape, p), None)
+                stage = [None] * P
+        staged = all(b is not None for b in stage)
         bufs = []
         for p in range(P):  # persistent per-pipeline device inputs (graph-captured addresses)
             b = self._inbufs.get((shape, p))
@@ -504,18 +521,21 @@ class LayerEvaluator:
             with torch.cuda.stream(copy[p]):
                 if s >= P:
                     copy[p].wait_event(consumed[p])
-                (stage[p] if packed else bufs[p]).copy_(host_inputs[s], non_blocking=True)
+                (stage[p] if staged else bufs[p]).copy_(host_inputs[s], non_blocking=True)
                 copied[p].record(copy[p])
             with torch.cuda.stream(comp[p]):
                 comp[p].wait_event(copied[p])
-                if packed:
-                    self.be.unpack_into(stage[p], bufs[p], level + 1)
+                if staged:
+                    if packed:
+                        self.be.unpack_into(stage[p], bufs[p], level + 1)
+                    else:
+                        bufs[p].copy_(stage[p], non_blocking=True)
                     consumed[p].record(comp[p])  # staging buffer free: next copy may start
                 if graphs:
                     out = self._replay(runners[p])
                 else:
                     out = self.run(enc, CipherBatch(bufs[p], level, scale, noise))
-                if not packed:
+                if not staged:
                     consumed[p].record(comp[p])
                 host_outputs[s].copy_(out.buf[:, :, : out.k], non_blocking=True)
                 if on_output is not None:
@@ -524,9 +544,9 @@ class LayerEvaluator:
             caller.wait_stream(st)
 
     def drop_input_buffers(self) -> None:
-        """Free the device staging buffers of bit-packed host inputs (``run_stream``); the
+        """Free the device staging buffers of host inputs (``run_stream``); the
         unpacked per-pipeline inputs stay (captured graphs hold their addresses)."""
-        for key in [k for k in self._inbufs if isinstance(k[0], tuple) and k[0][:1] == ("packed",)]:
+        for key in [k for k in self._inbufs if isinstance(k[0], tuple) and k[0][:1] in (("packed",), ("staged",))]:
             del self._inbufs[key]
 
     def run_many(self, enc: EncryptedNetworkBatch, x: CipherBatch, steps: int, pipelines: int = 2,
