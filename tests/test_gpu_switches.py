@@ -1,9 +1,9 @@
 """The library's run-time switches must not change a single bit.
 
 libheb200 reads its switches once per process (two-pass ModUp, FP64 engine off, ModUp
-target-set size, side streams), so every setting runs in its own subprocess: a seeded
-ct x ct multiply + relinearise + rescale and a rotation at N = 1024, 8192 and 32768
-(two levels) are hashed, and every switch must reproduce the default build's digests --
+target-set size, side streams, conv CTA width, conv split-limb body off), so every setting
+runs in its own subprocess: a seeded ct x ct multiply + relinearise + rescale, a rotation and
+a batched conv layer at N = 1024, 8192 and 32768 (two levels) are hashed, and every switch must reproduce the default build's digests --
 which `test_gpu_parity.py` / `test_gpu_invariants.py` pin to the oracle.
 """
 
@@ -23,6 +23,8 @@ warnings.simplefilter("ignore")
 sys.path.insert(0, %(repo)r)
 from paper_2102_00319_b200.backend import B200Backend
 from paper_2102_00319_b200.params import derive_params
+from paper_2102_00319_b200 import layers
+from paper_2102_00319_b200.model import Conv
 out = {}
 for m in (1 << 11, 1 << 14, 1 << 16):
     dev = B200Backend(derive_params(m, 180, 40, seed=3), 20)
@@ -36,6 +38,13 @@ for m in (1 << 11, 1 << 14, 1 << 16):
         c0, c1 = dev.cipher_rows_host(ct)
         h.update(np.ascontiguousarray(c0).tobytes())
         h.update(np.ascontiguousarray(c1).tobytes())
+    # a batched conv layer (2 filters 3x3 over a 4x4 grid): heb_conv_tensor + relinearise + rescale
+    imgs = rng.uniform(0, 1, (dev.slots, 4, 4))
+    wts = rng.normal(0, 0.3, (2, 1, 3, 3))
+    xb = layers.encrypt_images(dev, imgs, keys)
+    wb = dev.encrypt_batch(np.repeat(wts.ravel()[:, None], dev.slots, 1), keys, 1000 + np.arange(wts.size))
+    yc, _ = layers.LayerEvaluator(dev).conv(xb, (1, 4, 4), Conv(weights=wts, stride=1), wb, None)
+    h.update(yc.buf[:, :, : yc.k].cpu().numpy().tobytes())
     out[str(m)] = h.hexdigest()
 print("DIGESTS " + json.dumps(out))
 """
@@ -46,6 +55,9 @@ SWITCHES = [
     {"HEB_MODUP_TS": "1"},
     {"HEB_MODUP_TS": "99"},
     {"HEB_MODUP_CONCURRENT": "0", "HEB_MODDOWN_CONCURRENT": "0"},
+    {"HEB_CONV_NARROW": "0"},
+    {"HEB_CONV_NARROW": "1"},
+    {"HEB_CONV_NO_LIMBS": "1"},
 ]
 
 
