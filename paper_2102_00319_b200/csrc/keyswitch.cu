@@ -908,6 +908,12 @@ __global__ void k_cl_combine(Ctx K, const u64 *__restrict__ bL, const i64 *__res
     }
 }
 
+// ModDown tail at N = 2^15: forward transform over the parity split instead of the half split
+// (bit-exact; measured r2j, cfg4 tail ms per 4 steps: 173 -> 201: the DSMEM exchange and its
+// two cluster barriers cost more than the loader evaluated twice; off)
+#ifndef TAIL_EO
+#define TAIL_EO 0
+#endif
 template <int LOGN, int ENG>
 __global__ void ROW_BOUNDS(LOGN) k_ks_down_rescale_tail(Ctx K, const u64 *acc, heb_ct d, const i64 *aP, const i64 *cL,
                                                         int k, heb_ct out, int64_t count, int r0) {
@@ -940,7 +946,17 @@ __global__ void ROW_BOUNDS(LOGN) k_ks_down_rescale_tail(Ctx K, const u64 *acc, h
                 return (u64)__double_as_longlong(v);
             };
             constexpr int LL = Row<LOGN>::LL;
-            if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, 16, Row<LOGN>::SP>(fa, s2, twf, ld, y, rpart<LOGN>());
+            if constexpr (Row<LOGN>::SP == 2 && TAIL_EO) {
+                // parity split (see ntt::forward_split_eo): each CTA evaluates the loader for
+                // its own parity class only -- the half split evaluates it for both halves
+                // in both CTAs -- and the last stage crosses the pair through DSMEM
+                const int r = rpart<LOGN>();
+#pragma unroll 4
+                for (int jl = threadIdx.x; jl < (1 << LL); jl += KT<LOGN>)
+                    s2[ntt::pad(jl)] = __longlong_as_double((long long)ld(2 * jl + r));
+                __syncthreads();
+                ntt::forward_split_eo<LL, 16>(fa, s2, twf, y, r);
+            } else if constexpr (Row<LOGN>::SPLIT) ntt::forward_split<LL, 16, Row<LOGN>::SP>(fa, s2, twf, ld, y, rpart<LOGN>());
             else ntt::forward<LL, 16>(fa, s2, twf, ld, y);
             u64 x[16], z[16];
             load16<LOGN>(acc + ((b * 2 + c) * (k + 1) + i) * n + pos, x);
